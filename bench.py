@@ -1,0 +1,435 @@
+#!/usr/bin/env python
+"""DynLP per-batch update benchmark (BASELINE.json metric) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--config c2|c1|c3] [--n POINTS]
+
+A *step* is one engine.apply_batch (engine.py:328-413) over one batch of the
+synthetic stream, all label columns (C2: 10 one-vs-rest columns).  The
+stream is built with the make_stream rules (stream.py:56-183) from Gaussian
+blobs and their cosine k-NN graph (builder.py:42-92 semantics; k-NN computed
+on the GPU for input generation only).  Batches before the warm-up window
+are a bootstrap (setup, untimed); the W warm-up batches and the K timed
+batches are the last W+K batches of the stream (|V| ~ 0.9M..1M at C2).
+
+Legs (one process per GPU; N > 1 runs N independent replicas = weak scaling):
+  value  device-resident batches (pre-uploaded), dlp_apply_batch_device
+  e2e    host numpy batches through the public API (H2D inside each step),
+         report copied back to the host every step
+  cpu_baseline  the reference CPU path on a bounded sample: state hand-off of
+         the GPU labels before the first timed batch, structure replay, then
+         one label column of that batch timed on all host threads.
+--impl reference times the reference's CPU path alone on the same workload
+(rank 0 only): oracle/_ref (the compiled reference) when importable, else
+the C restatement in oracle/.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # BASELINE.json configs[1]: 1M x 128, 10 classes, k=10, 1% seeds, 100 insert batches of 10k
+    "c2": dict(n=1_000_000, dim=128, classes=10, k=10, seed_frac=0.01, batch=10_000,
+               fractions=(0.99, 0.01, 0.0), seed=0, delta=1e-4,
+               desc="C2: synthetic blobs 1M x 128-dim, 10 classes (one-vs-rest columns), "
+                    "cosine kNN k=10, 1% seeds, 100 insert batches of 10k"),
+    # configs[0]: 10k x 16, 3 classes, k=10, 1% seeds, batches of 500
+    "c1": dict(n=10_000, dim=16, classes=3, k=10, seed_frac=0.01, batch=500,
+               fractions=(0.99, 0.01, 0.0), seed=0, delta=1e-4,
+               desc="C1: synthetic blobs 10k x 16-dim, 3 classes, kNN k=10, 1% seeds, batches of 500"),
+    # configs[2]: the C2 graph statistics with mixed 70/30 insert/delete batches
+    "c3": dict(n=1_000_000, dim=128, classes=10, k=10, seed_frac=0.01, batch=10_000,
+               fractions=(0.69, 0.01, 0.30), seed=0, delta=1e-4,
+               desc="C3: blobs 1M x 128, 10 classes, kNN k=10, mixed batches 69/1/30 "
+                    "insert/gt/delete of 10k"),
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def make_stream(cfg, device):
+    from paper_2604_06596_b200 import streams
+
+    cache_dir = os.environ.get("DYNLP_BENCH_CACHE", "/tmp/dynlp_bench_cache")
+    os.makedirs(cache_dir, exist_ok=True)
+    key = "_".join(str(cfg[k]) for k in ("n", "dim", "classes", "k", "seed_frac", "batch", "seed")) + \
+        "_" + "_".join(str(x) for x in cfg["fractions"])
+    path = os.path.join(cache_dir, f"stream_{key}.npz")
+    if os.path.exists(path):
+        z = np.load(path)
+        from paper_2604_06596_b200.batch import BatchUpdate
+
+        io, eo, do = z["io"], z["eo"], z["do"]
+        batches = [BatchUpdate(t=t, insert_ids=z["ids"][io[t]:io[t + 1]], insert_gt=z["gt"][io[t]:io[t + 1]],
+                               edge_owner=z["own"][eo[t]:eo[t + 1]], edge_other=z["oth"][eo[t]:eo[t + 1]],
+                               edge_w=z["w"][eo[t]:eo[t + 1]], deletes=z["dels"][do[t]:do[t + 1]])
+                   for t in range(len(io) - 1)]
+        return batches, z["classes"]
+    t0 = time.time()
+    bl = streams.make_blobs(cfg["n"], cfg["dim"], cfg["classes"], cfg["seed"], dtype=np.float32)
+    if device is not None and cfg["n"] > 20_000:
+        import torch
+
+        torch.backends.cuda.matmul.allow_tf32 = True
+        edges = streams.knn_graph_torch(bl.x, cfg["k"], device=device, block=4096)
+    else:
+        edges = streams.knn_graph_exact(bl.x.astype(np.float64), cfg["k"])
+    gt = streams.stratified_seeds(bl.classes, cfg["seed_frac"], cfg["seed"])
+    fi, fg, fd = cfg["fractions"]
+    if fd > 0:
+        # phase 1 (bootstrap) grows the graph to n_target with inserts, phase 2 is mixed
+        phases = [(cfg["n_boot_batches"], cfg["batch"], 0.99, 0.01, 0.0),
+                  (None, cfg["batch"], fi, fg, fd)]
+    else:
+        phases = None
+    s = streams.phased_stream(cfg["n"], edges, bl.classes, gt, cfg["batch"], cfg["seed"], fi, fg, fd,
+                              initial_gt=2 * cfg["classes"], phases=phases)
+    log(f"[bench] stream built in {time.time() - t0:.1f}s: {len(s.batches)} batches, "
+        f"{len(edges)} kNN edges")
+    b = s.batches
+    np.savez(path, ids=np.concatenate([x.insert_ids for x in b]), gt=np.concatenate([x.insert_gt for x in b]),
+             own=np.concatenate([x.edge_owner for x in b]), oth=np.concatenate([x.edge_other for x in b]),
+             w=np.concatenate([x.edge_w for x in b]), dels=np.concatenate([x.deletes for x in b]),
+             io=np.cumsum([0] + [len(x.insert_ids) for x in b]),
+             eo=np.cumsum([0] + [len(x.edge_owner) for x in b]),
+             do=np.cumsum([0] + [len(x.deletes) for x in b]), classes=s.classes)
+    return s.batches, s.classes
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "200",
+                 "-i", str(self.index)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 8:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx = max(mx, float(p[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def remap_gt(b, c, ncol):
+    if ncol == 1:
+        return b
+    from paper_2604_06596_b200.batch import BatchUpdate
+
+    g = np.asarray(b.insert_gt)
+    return BatchUpdate(b.t, b.insert_ids, np.where(g < 0, -1, np.where(g == c, 1, 0)).astype(np.int8),
+                       b.edge_owner, b.edge_other, b.edge_w, b.deletes)
+
+
+def cpu_reference_run(batches, t0, steps, F0, ncol, delta, threads, column=0, kind=None):
+    """Time the reference CPU path on batches t0..t0+steps-1 for one label
+    column, starting from the hand-off labels F0 (state before batch t0).
+    Returns (kind, per-step seconds, per-step (iterations, updates, max_change))."""
+    from oracle import OracleEngine, load_reference
+
+    ref = None if kind == "port" else load_reference()
+    times, reps = [], []
+    if ref is not None:
+        from dynlp.engine import EngineConfig, apply_batch, apply_batch_structure
+        from dynlp.graph import BatchUpdate as RB
+        from dynlp.graph import DynamicGraph
+        from dynlp.labels import LabelState
+
+        def rb(b):
+            b = remap_gt(b, column, ncol)
+            return RB(int(b.t), np.asarray(b.insert_ids), np.asarray(b.insert_gt), np.asarray(b.edge_owner),
+                      np.asarray(b.edge_other), np.asarray(b.edge_w), np.asarray(b.deletes))
+
+        g, lab = DynamicGraph(), LabelState()
+        for b in batches[:t0]:
+            apply_batch_structure(g, lab, rb(b))
+        lab.f[: g.num_slots] = F0[column][: g.num_slots]
+        cfg = EngineConfig(delta=delta, threads=threads)
+        for b in batches[t0:t0 + steps]:
+            s = time.perf_counter()
+            lab, r = apply_batch(g, lab, rb(b), cfg)
+            times.append(time.perf_counter() - s)
+            reps.append((r.iterations, r.updates, r.max_change))
+        return "reference", times, reps
+    orc = OracleEngine(2, threads=threads)
+    for b in batches[:t0]:
+        orc.apply_structure(remap_gt(b, column, ncol))
+    orc.write_labels(F0[column][: orc.num_slots][None, :])
+    for b in batches[t0:t0 + steps]:
+        s = time.perf_counter()
+        (r,) = orc.apply_batch(remap_gt(b, column, ncol), delta=delta)
+        times.append(time.perf_counter() - s)
+        reps.append((r.iterations, r.updates, r.max_change))
+    return "port", times, reps
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def traffic_record():
+    p = os.path.join(ROOT, "profiles", "lp_kernel_traffic.json")
+    if os.path.exists(p):
+        try:
+            return json.load(open(p))
+        except Exception:
+            return None
+    return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--n", type=int, default=None, help="override point count (smaller smoke runs)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-kind", default=None, choices=[None, "reference", "port"])
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    cfg = dict(CONFIGS[args.config])
+    if args.n:
+        cfg["n"] = args.n
+    n_batches_total = None
+
+    import torch
+
+    have_gpu = torch.cuda.is_available()
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl" if have_gpu else "gloo")
+    if args.impl == "reference" and rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+    device = f"cuda:{local}" if have_gpu else None
+    if have_gpu:
+        torch.cuda.set_device(local)
+
+    if cfg["fractions"][2] > 0:
+        cfg["n_boot_batches"] = max(1, int(0.6 * cfg["n"] / cfg["batch"]))
+    batches, classes = make_stream(cfg, device)
+    T = len(batches)
+    K, W = args.steps, args.warmup
+    t0 = T - K  # first timed batch
+    tw = t0 - W  # first warm-up batch
+    if tw < 1:
+        raise SystemExit(f"stream has {T} batches; need more than steps+warmup")
+    ncol = 1 if cfg["classes"] <= 2 else cfg["classes"]
+    delta = cfg["delta"]
+
+    from paper_2604_06596_b200.engine import DynamicGraph, EngineConfig, LabelState, apply_batch
+
+    ecfg = EngineConfig(delta=delta)
+    threads = os.cpu_count() or 1
+
+    def bootstrap():
+        g, lab = DynamicGraph(local, num_classes=max(2, cfg["classes"])), LabelState()
+        s = time.time()
+        for b in batches[:tw]:
+            apply_batch(g, lab, b, ecfg)
+        for b in batches[tw:t0]:  # warm-up steps (untimed)
+            apply_batch(g, lab, b, ecfg)
+        log(f"[bench] rank {rank}: bootstrap+warmup {t0} batches in {time.time() - s:.1f}s, |V|={g.num_slots}")
+        return g, lab
+
+    if args.impl == "reference":
+        g, lab = bootstrap()  # GPU used only to produce the hand-off label state (untimed)
+        F0 = lab.F.copy()
+        g.close()
+        kind, times, reps = cpu_reference_run(batches, t0, K, F0, ncol, delta, threads, kind=args.cpu_kind)
+        per_col_ms = 1e3 * float(np.mean(times))
+        val = per_col_ms * ncol
+        line = {"impl": "reference", "metric": "dynlp_ms_per_batch", "value": val, "unit": "ms/batch",
+                "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": val, "higher_is_better": False,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": cfg["desc"], "timed_batches": f"t={t0}..{T - 1}"},
+                "cpu_baseline": {"value": val, "unit": "ms/batch", "cores": threads, "kind": kind,
+                                 "sample": f"label column 0 of {ncol} (one-vs-rest) for each of batches "
+                                           f"t={t0}..{t0 + K - 1}, state hand-off at t={t0}; "
+                                           f"ms/batch = column time x {ncol}"},
+                "e2e": {"value": val, "unit": "ms/batch", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+                "cpu_reports": reps}
+        print(json.dumps(line), flush=True)
+        if dist:
+            dist.destroy_process_group()
+        return
+
+    # ---------------- B200 arm -----------------------------------------------------
+    gA, labA = bootstrap()
+    F0 = labA.F.copy() if rank == 0 and not args.no_cpu_baseline else None
+    # device-resident batches for the value leg
+    dev = []
+    for b in batches[t0:]:
+        dev.append(dict(t=b.t, n_ins=len(b.insert_ids), n_edges=len(b.edge_owner), n_del=len(b.deletes),
+                        insert_ids=torch.as_tensor(np.asarray(b.insert_ids, np.int64), device=device),
+                        insert_gt=torch.as_tensor(np.asarray(b.insert_gt, np.int8), device=device),
+                        edge_owner=torch.as_tensor(np.asarray(b.edge_owner, np.int64), device=device),
+                        edge_other=torch.as_tensor(np.asarray(b.edge_other, np.int64), device=device),
+                        edge_w=torch.as_tensor(np.asarray(b.edge_w, np.float64), device=device),
+                        deletes=torch.as_tensor(np.asarray(b.deletes, np.int64), device=device)))
+    torch.cuda.synchronize()
+
+    def barrier():
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if not dist:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    clocks = ClockSampler(local)
+    # ---- value leg: inputs resident in HBM --------------------------------------
+    barrier()
+    clocks.start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    repsA = []
+    for s in range(K):
+        repsA.append(gA.apply_device(dev[s], ecfg, trusted=True))
+    ev1.record()
+    barrier()
+    clk = clocks.stop()
+    ms_value = max_over_ranks(ev0.elapsed_time(ev1)) / K
+    gA.close()
+
+    # ---- e2e leg: host buffers through the public API ---------------------------
+    gB, labB = bootstrap()
+    h2d = sum(b.insert_ids.nbytes + b.insert_gt.nbytes + b.edge_owner.nbytes + b.edge_other.nbytes +
+              b.edge_w.nbytes + b.deletes.nbytes for b in batches[t0:]) // K
+    d2h = 0
+    barrier()
+    ev0.record()
+    repsB = []
+    for b in batches[t0:]:
+        labB, r = apply_batch(gB, labB, b, ecfg)
+        repsB.append(r if isinstance(r, list) else [r])
+        d2h = ctypes_report_bytes(ncol)
+    ev1.record()
+    barrier()
+    ms_e2e = max_over_ranks(ev0.elapsed_time(ev1)) / K
+    gB.close()
+
+    # ---- aggregates -------------------------------------------------------------
+    upd = sum(r.updates for step in repsA for r in step)
+    edges = sum(r.edges_traversed for step in repsA for r in step)
+    lp_ms = sum(r.lp_kernel_ms for step in repsA for r in step)
+    launches = sum(step[-1].gpu_launches for step in repsA) / K
+    alg_bytes = 32.0 * upd + 21.0 * edges
+    achieved = alg_bytes / (lp_ms * 1e-3) / 1e9 if lp_ms > 0 else None
+    peak, peak_kind = measured_peaks()
+    tr = traffic_record()
+    same = all(a[c].iterations == b[c].iterations and a[c].updates == b[c].updates
+               for a, b in zip(repsA, repsB) for c in range(len(a)))
+    line = {
+        "metric": "dynlp_ms_per_batch", "value": ms_value, "unit": "ms/batch", "n_gpus": world,
+        "steps": K, "warmup": W, "ms_per_step": ms_value, "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg["desc"], "points": cfg["n"], "timed_batches": f"t={t0}..{T - 1}",
+                   "label_columns": ncol, "delta": delta, "parallelism": f"replicas x{world}",
+                   "l2": "no flush: per-batch working set (adjacency ~200 MB + 10 label columns) exceeds "
+                         "the 126 MB L2"},
+        "edges_per_s": edges / (ms_value * K * 1e-3),
+        "vertex_updates_per_batch": upd / K, "edge_relaxations_per_batch": edges / K,
+        "lp_kernel_share": lp_ms / (ms_value * K),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": (achieved / peak) if achieved else None,
+                     "traffic": (tr or {}).get("dram_bytes_per_alg_byte"),
+                     "kernel": "k_lp_loop (persistent frontier/certify loop)",
+                     "algorithmic_bytes": "32 B/vertex-update + 21 B/edge-entry (SURVEY §8(d) D-4)",
+                     "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})"},
+        "e2e": {"value": ms_e2e, "unit": "ms/batch", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h)},
+        "gpu_launches": launches, "clocks": clk,
+        "legs_identical_work": same,
+    }
+    if rank == 0 and not args.no_cpu_baseline:
+        kind, times, reps = cpu_reference_run(batches, t0, 1, F0, ncol, delta, threads, kind=args.cpu_kind)
+        gpu_col0 = repsA[0][0]
+        cpu_ms = 1e3 * times[0] * ncol
+        line["cpu_baseline"] = {
+            "value": cpu_ms, "unit": "ms/batch", "cores": threads, "kind": kind,
+            "sample": f"label column 0 of {ncol} for batch t={t0} (state hand-off from the GPU at t={t0}), "
+                      f"x{ncol} columns",
+            "parity_with_gpu": list(reps[0][:2]) == [gpu_col0.iterations, gpu_col0.updates]
+                               and reps[0][2] == gpu_col0.max_change,
+            "speedup_vs_value": cpu_ms / ms_value, "speedup_vs_e2e": cpu_ms / ms_e2e}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def ctypes_report_bytes(ncol):
+    from paper_2604_06596_b200 import _native
+    import ctypes
+
+    return ctypes.sizeof(_native.Report) * ncol
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,154 @@
+/*
+ * dynlp_b200.h -- C ABI of the B200-native DynLP batch-update engine.
+ *
+ * Plain C types only (no torch, no CUDA types), so any FFI (ctypes, cgo,
+ * JNI, N-API) can bind it.  Every entry point cites the reference interface
+ * it replaces (paths relative to /root/reference/pkg/src/dynlp/).
+ *
+ * Ownership: the engine owns all device memory (graph,
+ * labels, component state) and keeps it resident across calls.  Batch and
+ * read-out pointers are borrowed for the duration of one call.  Calls are
+ * synchronous: they return after the report is on the host.
+ *
+ * Status codes (B4): 0 ok, 3 validation (-> dynlp.errors.ValidationError; the
+ * engine state is unchanged), 4 format, 5 CUDA, 6 internal.  The message of
+ * the last failure is available from dlp_last_error().  Non-convergence is
+ * not an error (report.converged = 0).
+ */
+#ifndef DYNLP_B200_H
+#define DYNLP_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DLP_OK 0
+#define DLP_EVALIDATION 3
+#define DLP_EFORMAT 4
+#define DLP_ECUDA 5
+#define DLP_EINTERNAL 6
+
+#define DLP_MODE_JACOBI 0       /* engine.py:33 "parallel_jacobi" */
+#define DLP_MODE_GAUSS_SEIDEL 1 /* engine.py:34 "sequential_gauss_seidel" */
+
+typedef struct dlp_engine dlp_engine;
+
+/* EngineConfig (engine.py:40-70).  threads is meaningless on the device and
+ * is not carried; num_classes > 2 selects one-vs-rest label columns. */
+typedef struct {
+    double delta;           /* engine.py:42; must be > 0 */
+    double tau;             /* engine.py:43; NaN = "auto" (mean live weight) */
+    int64_t max_iterations; /* engine.py:44; <= 0 = 10 * num_alive (engine.py:67-70) */
+    int32_t component_init; /* engine.py:47 */
+    int32_t mode;           /* DLP_MODE_* */
+    int32_t num_classes;    /* 2 = binary (reference); C > 2 = C columns */
+    int32_t reserved;
+} dlp_config;
+
+/* BatchUpdate (graph.py:67-82): edge_owner indexes insert_ids. */
+typedef struct {
+    int64_t t;
+    int64_t n_ins;
+    const int64_t* insert_ids;
+    const int8_t* insert_gt; /* -1 unlabeled, else class */
+    int64_t n_edges;
+    const int64_t* edge_owner;
+    const int64_t* edge_other;
+    const double* edge_w;
+    int64_t n_del;
+    const int64_t* deletes;
+} dlp_batch;
+
+/* IterationReport (engine.py:104-115) + device counters. */
+typedef struct {
+    int64_t t;
+    int64_t iterations;
+    int64_t updates;
+    double max_change;
+    int32_t converged;
+    int32_t pad;
+    int64_t warnings;
+    int64_t isolated_pinned;
+    int64_t unreachable_pinned;
+    double wall_time_ms;
+    int64_t edges_traversed; /* sum of row lengths over every vertex update */
+    int64_t certify_sweeps;
+    double lp_kernel_ms;     /* CUDA-event time of this column's propagation kernel */
+    int64_t gpu_launches;    /* kernels this call launched so far (all columns) */
+} dlp_report;
+
+/* Engine lifetime: replaces DynamicGraph() + LabelState() (graph.py:179,
+ * labels.py:20) -- an empty graph on `device`. */
+int dlp_create(const dlp_config* cfg, int device, dlp_engine** out);
+int dlp_destroy(dlp_engine* e);
+const char* dlp_last_error(dlp_engine* e);
+int dlp_num_columns(dlp_engine* e);
+
+/* engine.apply_batch (engine.py:328-413) with HOST batch arrays.  Writes one
+ * report per label column (1 for binary).  cfg may differ between calls
+ * (delta / tau / max_iterations / component_init / mode); num_classes is
+ * fixed at dlp_create. */
+int dlp_apply_batch(dlp_engine* e, const dlp_config* cfg, const dlp_batch* batch,
+                    dlp_report* reports);
+/* Same, batch arrays already resident in device memory (bench "value" leg).
+ * Validation still runs against the engine's host mirror, so the arrays are
+ * also read back for it unless `trusted` is nonzero. */
+int dlp_apply_batch_device(dlp_engine* e, const dlp_config* cfg, const dlp_batch* dev_batch,
+                           int trusted, dlp_report* reports);
+/* engine.apply_batch_structure (engine.py:141-156): deletes, inserts, ground
+ * truth; no propagation.  Also used for CPU-baseline state hand-off. */
+int dlp_apply_structure(dlp_engine* e, const dlp_batch* batch);
+/* baselines.itlp_batch_solve (baselines.py:236-253): structure, then full
+ * Jacobi sweeps over alive unlabeled vertices with positive degree. */
+int dlp_itlp_batch(dlp_engine* e, const dlp_config* cfg, const dlp_batch* batch,
+                   dlp_report* reports);
+
+/* DynamicGraph.num_slots / num_alive (graph.py:189-192, 182). */
+int dlp_num_slots(dlp_engine* e, int64_t* n_slots, int64_t* num_alive);
+/* LabelState.f / .gt (labels.py:21-22).  f is [columns][n] row-major; GT
+ * vertices read as their pinned class value.  n must equal num_slots. */
+int dlp_read_labels(dlp_engine* e, double* f, int8_t* gt, int64_t n);
+/* Overwrite f (CPU-baseline hand-off and tests); GT entries are ignored. */
+int dlp_write_labels(dlp_engine* e, const double* f, int64_t n);
+int dlp_read_alive(dlp_engine* e, uint8_t* alive, int64_t n);
+/* eligible mask of the last batch (engine.py:361), before the loop. */
+int dlp_read_eligible(dlp_engine* e, uint8_t* eligible, int64_t n);
+/* number of live undirected edges and the tau resolved by the last batch */
+int dlp_graph_stats(dlp_engine* e, int64_t* live_edges, double* last_tau);
+/* DynamicGraph.csr() snapshot (graph.py:218-231): indptr[n+1], indices and
+ * weights [nnz = 2 * live_edges], degrees [n] (row-order sums). */
+int dlp_read_csr(dlp_engine* e, int64_t* indptr, int64_t* indices, double* weights,
+                 double* degrees, int64_t n, int64_t nnz);
+/* live_edges() in log order (graph.py:205-216). */
+int dlp_read_live_edges(dlp_engine* e, int64_t* u, int64_t* v, double* w, int64_t m);
+/* find_components labeling of the last batch (components.py:84-124):
+ * vertices (sorted), parent (min member id), component_id (dense). */
+int dlp_read_intra(dlp_engine* e, int64_t* vertices, int64_t* parent, int64_t* comp,
+                   int64_t cap, int64_t* k);
+
+/* Kernel plugin API: dynlp.kernels (kernels/__init__.py:28-30) with the
+ * signatures of kernels/_csr.pyx:61-70, 94-102, 114-125 on HOST arrays. */
+int dlp_jacobi_step(const int64_t* indptr, const int64_t* indices, const double* weights,
+                    const int8_t* gt, const double* f, int64_t n, const int64_t* frontier,
+                    int64_t nf, double* out_vals, double* out_deltas);
+int dlp_gauss_seidel_step(const int64_t* indptr, const int64_t* indices, const double* weights,
+                          const int8_t* gt, double* f, int64_t n, const int64_t* frontier,
+                          int64_t nf, double* out_deltas);
+/* leftover (capacity max(n, nf)) is returned sorted ascending. */
+int dlp_jacobi_run(const int64_t* indptr, const int64_t* indices, const double* weights,
+                   const int8_t* gt, double* f, int64_t n, const int64_t* frontier_init,
+                   int64_t nf, uint8_t* eligible, double delta, int64_t max_iters,
+                   int64_t* out_iters, int64_t* out_updates, double* out_max_change,
+                   int64_t* out_warnings, int64_t* leftover, int64_t* n_leftover);
+const char* dlp_plugin_last_error(void);
+
+/* Device / build facts for reports: SM count and whether the sm_100a image
+ * is loadable on the current device. */
+int dlp_device_info(int device, int* sm_count, int* cc_major, int* cc_minor);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,583 @@
+// abi.cu -- C-ABI entry points (include/dynlp_b200.h) and the host-side
+// orchestration of one batch: validate on the host mirror, stage the batch,
+// enqueue the device pipeline, read the report back.
+//
+// engine.apply_batch (engine.py:328-413) order of operations:
+//   validate (graph.py:254-309) -> deletes -> inserts + ground truth
+//   -> tau -> intra-batch components + initialisation -> reachability, pin,
+//   eligible -> per label column: frontier rounds / certify sweeps.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "engine.cuh"
+
+using namespace dlp;
+
+struct dlp_engine {
+    Engine E;
+    bool poisoned = false;
+};
+
+namespace {
+
+int fail(Engine& E, int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    E.err = buf;
+    return code;
+}
+
+int cuda_fail(dlp_engine* h, const CudaFailure& f) {
+    h->poisoned = true;
+    return fail(h->E, DLP_ECUDA, "CUDA error %s at %s:%d (%s)", cudaGetErrorString(f.err), f.file, f.line, f.expr);
+}
+
+int check_config(Engine& E, const dlp_config* c) {
+    // EngineConfig.validate (engine.py:49-60)
+    if (!(c->delta > 0)) return fail(E, DLP_EVALIDATION, "delta must be positive");
+    if (c->mode != DLP_MODE_JACOBI && c->mode != DLP_MODE_GAUSS_SEIDEL)
+        return fail(E, DLP_EVALIDATION, "unknown mode %d", c->mode);
+    if (!std::isnan(c->tau) && c->tau < 0) return fail(E, DLP_EVALIDATION, "tau must be nonnegative");
+    return DLP_OK;
+}
+
+struct HostBatch {
+    long long t, k, ne, nd;
+    const long long *ids, *owner, *other, *dels;
+    const signed char* gt;
+    const double* w;
+};
+
+// DynamicGraph.validate_batch (graph.py:306-309): validate_deletes then
+// validate_inserts with pending deletes; same checks, order and messages.
+int validate_batch(Engine& E, const HostBatch& b) {
+    long long n = E.n_slots;
+    if (b.nd) {
+        std::vector<long long> d(b.dels, b.dels + b.nd);
+        std::sort(d.begin(), d.end());
+        for (long long i = 1; i < b.nd; i++)
+            if (d[i] == d[i - 1]) return fail(E, DLP_EVALIDATION, "duplicate vertex id in deletes");
+        for (long long x : d)
+            if (x < 0 || x >= n) return fail(E, DLP_EVALIDATION, "unknown vertex id %lld in deletes", x);
+        for (long long x : d)
+            if (!E.h_alive[x]) return fail(E, DLP_EVALIDATION, "vertex %lld is already deleted", x);
+    }
+    long long k = b.k;
+    if (k == 0) {
+        if (b.ne) return fail(E, DLP_EVALIDATION, "batch has edges but no inserted vertices");
+        return DLP_OK;
+    }
+    {
+        std::vector<long long> ids(b.ids, b.ids + k);
+        std::sort(ids.begin(), ids.end());
+        for (long long i = 1; i < k; i++)
+            if (ids[i] == ids[i - 1]) return fail(E, DLP_EVALIDATION, "duplicate fresh id in inserts");
+        for (long long i = 0; i < k; i++)
+            if (ids[i] != n + i)
+                return fail(E, DLP_EVALIDATION, "insert ids must be the contiguous block %lld..%lld", n, n + k - 1);
+    }
+    for (long long i = 0; i < b.nd; i++)
+        if (b.dels[i] >= n && b.dels[i] < n + k)
+            return fail(E, DLP_EVALIDATION, "a vertex id appears in both inserts and deletes");
+    if (b.ne) {
+        for (long long j = 0; j < b.ne; j++)
+            if (b.w[j] < 0) return fail(E, DLP_EVALIDATION, "negative weight on edge to vertex %lld", b.other[j]);
+        for (long long j = 0; j < b.ne; j++) {
+            if (b.owner[j] < 0 || b.owner[j] >= k)
+                return fail(E, DLP_EVALIDATION, "edge owner index %lld out of range", b.owner[j]);
+            if (b.ids[b.owner[j]] == b.other[j]) return fail(E, DLP_EVALIDATION, "self-loop in insert edges");
+        }
+        for (long long j = 0; j < b.ne; j++) {
+            long long o = b.other[j];
+            if (o >= n && o < n + k) continue;
+            if (o < 0 || o >= n) return fail(E, DLP_EVALIDATION, "edge to unknown vertex %lld", o);
+        }
+        for (long long j = 0; j < b.ne; j++) {
+            long long o = b.other[j];
+            if (o >= n && o < n + k) continue;
+            if (!E.h_alive[o]) return fail(E, DLP_EVALIDATION, "edge to a dead vertex %lld", o);
+        }
+        if (b.nd) {
+            std::vector<unsigned char> pend(n + 1, 0);
+            for (long long i = 0; i < b.nd; i++) pend[b.dels[i]] = 1;
+            for (long long j = 0; j < b.ne; j++) {
+                long long o = b.other[j];
+                if (o >= n && o < n + k) continue;
+                if (pend[o]) return fail(E, DLP_EVALIDATION, "edge to vertex %lld deleted in the same batch", o);
+            }
+        }
+    }
+    // LabelState.set_ground_truth class check (labels.py:42-43), hoisted
+    // before any mutation so a bad class cannot half-apply a batch.
+    for (long long i = 0; i < k; i++) {
+        int g = b.gt[i];
+        if (g < -1 || g >= E.num_classes) {
+            if (E.num_classes == 2) return fail(E, DLP_EVALIDATION, "ground-truth class must be 0 or 1");
+            return fail(E, DLP_EVALIDATION, "ground-truth class must be in [0, %d)", E.num_classes);
+        }
+    }
+    return DLP_OK;
+}
+
+__global__ void k_reset_batch(DevState* ds) {
+    ds->m_kept = 0;
+    ds->n_purge = 0;
+    ds->n_touched = 0;
+    ds->n_f0 = 0;
+    ds->n_elist = 0;
+    ds->isolated = 0;
+    ds->unreach = 0;
+    ds->intra_nc = 0;
+}
+
+size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+// Stage host batch arrays into one pinned buffer and copy it to the device.
+BatchDev stage_batch(Engine& E, const HostBatch& b) {
+    size_t off[7];
+    size_t sz[6] = {(size_t)b.k * 8, (size_t)b.k, (size_t)b.ne * 8, (size_t)b.ne * 8, (size_t)b.ne * 8, (size_t)b.nd * 8};
+    size_t tot = 0;
+    for (int i = 0; i < 6; i++) {
+        off[i] = tot;
+        tot += align_up(sz[i]);
+    }
+    off[6] = tot;
+    E.h_stage.reserve(tot + 256);
+    E.d_stage.reserve(tot + 256, 0, E.st);
+    const void* src[6] = {b.ids, b.gt, b.owner, b.other, b.w, b.dels};
+    for (int i = 0; i < 6; i++)
+        if (sz[i]) memcpy(E.h_stage.p + off[i], src[i], sz[i]);
+    if (tot) DLP_CUDA_TRY(cudaMemcpyAsync(E.d_stage.p, E.h_stage.p, tot, cudaMemcpyHostToDevice, E.st));
+    unsigned char* d = E.d_stage.p;
+    BatchDev bd;
+    bd.ids = (const long long*)(d + off[0]);
+    bd.gt = (const signed char*)(d + off[1]);
+    bd.owner = (const long long*)(d + off[2]);
+    bd.other = (const long long*)(d + off[3]);
+    bd.w = (const double*)(d + off[4]);
+    bd.dels = (const long long*)(d + off[5]);
+    bd.k = b.k;
+    bd.ne = b.ne;
+    bd.nd = b.nd;
+    return bd;
+}
+
+enum Kind { KIND_DYNLP = 0, KIND_STRUCTURE = 1, KIND_ITLP = 2 };
+
+int run_batch(dlp_engine* h, const dlp_config* cfg, const dlp_batch* batch, bool device_ptrs, bool trusted,
+              dlp_report* reps, Kind kind) {
+    Engine& E = h->E;
+    auto t0 = std::chrono::steady_clock::now();
+    if (h->poisoned) return fail(E, DLP_EINTERNAL, "engine is unusable after an earlier CUDA error");
+    if (cfg) {
+        int rc = check_config(E, cfg);
+        if (rc) return rc;
+        if (cfg->mode == DLP_MODE_GAUSS_SEIDEL && kind == KIND_DYNLP)
+            return fail(E, DLP_EVALIDATION, "mode 'sequential_gauss_seidel' is not supported by the B200 engine");
+    }
+    if (reps)
+        for (int c = 0; c < E.ncol; c++) {
+            memset(&reps[c], 0, sizeof(dlp_report));
+            reps[c].t = batch->t;
+            reps[c].converged = 1;
+        }
+    auto finish_time = [&]() {
+        double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        if (reps)
+            for (int c = 0; c < E.ncol; c++) reps[c].wall_time_ms = ms;
+    };
+    if (batch->n_ins == 0 && batch->n_del == 0 && kind != KIND_ITLP) {  // engine.py:338-340
+        finish_time();
+        return DLP_OK;
+    }
+    // host views (read back device batches for validation unless trusted)
+    std::vector<long long> hv_ids, hv_owner, hv_other, hv_dels;
+    std::vector<signed char> hv_gt;
+    std::vector<double> hv_w;
+    HostBatch hb{batch->t,
+                 batch->n_ins,
+                 batch->n_edges,
+                 batch->n_del,
+                 (const long long*)batch->insert_ids,
+                 (const long long*)batch->edge_owner,
+                 (const long long*)batch->edge_other,
+                 (const long long*)batch->deletes,
+                 (const signed char*)batch->insert_gt,
+                 batch->edge_w};
+    try {
+        DLP_CUDA_TRY(cudaSetDevice(E.device));
+        if (device_ptrs && !trusted) {
+            auto pull = [&](auto& vec, const void* src, size_t n) {
+                vec.resize(n);
+                if (n) DLP_CUDA_TRY(cudaMemcpy(vec.data(), src, n * sizeof(vec[0]), cudaMemcpyDeviceToHost));
+            };
+            pull(hv_ids, batch->insert_ids, batch->n_ins);
+            pull(hv_gt, batch->insert_gt, batch->n_ins);
+            pull(hv_owner, batch->edge_owner, batch->n_edges);
+            pull(hv_other, batch->edge_other, batch->n_edges);
+            pull(hv_w, batch->edge_w, batch->n_edges);
+            pull(hv_dels, batch->deletes, batch->n_del);
+            hb.ids = hv_ids.data();
+            hb.gt = hv_gt.data();
+            hb.owner = hv_owner.data();
+            hb.other = hv_other.data();
+            hb.w = hv_w.data();
+            hb.dels = hv_dels.data();
+        }
+        if (!(device_ptrs && trusted)) {
+            int rc = validate_batch(E, hb);
+            if (rc) return rc;
+        }
+        long long base = E.n_slots, k = hb.k, ne = hb.ne, nd = hb.nd;
+        ensure_vertex_capacity(E, base + k + 1);
+        ensure_log(E, E.live_edges + ne + 1);
+        ensure_pool(E, ne, k);
+        BatchDev bd;
+        if (device_ptrs) {
+            bd.ids = (const long long*)batch->insert_ids;
+            bd.gt = (const signed char*)batch->insert_gt;
+            bd.owner = (const long long*)batch->edge_owner;
+            bd.other = (const long long*)batch->edge_other;
+            bd.w = batch->edge_w;
+            bd.dels = (const long long*)batch->deletes;
+            bd.k = k;
+            bd.ne = ne;
+            bd.nd = nd;
+        } else {
+            bd = stage_batch(E, hb);
+        }
+        long long launches0 = E.launches;
+        k_reset_batch<<<1, 1, 0, E.st>>>(E.ds);
+        E.launches++;
+        apply_deletes_dev(E, bd);
+        apply_inserts_dev(E, bd, base);
+        // host mirror of alive (validation of later batches)
+        if (nd) {
+            if (!(device_ptrs && trusted)) {
+                for (long long i = 0; i < nd; i++) E.h_alive[hb.dels[i]] = 0;
+            } else {
+                std::vector<long long> dd(nd);
+                DLP_CUDA_TRY(cudaMemcpy(dd.data(), batch->deletes, nd * 8, cudaMemcpyDeviceToHost));
+                for (long long x : dd) E.h_alive[x] = 0;
+            }
+        }
+        E.h_alive.resize(base + k, 1);
+        E.n_slots = base + k;
+        E.num_alive += k - nd;
+        long long n = E.n_slots;
+        if (kind == KIND_STRUCTURE) {
+            DLP_CUDA_TRY(cudaMemcpyAsync(E.h_ds.p, E.ds, sizeof(DevState), cudaMemcpyDeviceToHost, E.st));
+            DLP_CUDA_TRY(cudaStreamSynchronize(E.st));
+            E.live_edges = E.h_ds.p->log_n;
+            E.pool_top_host = (long long)E.h_ds.p->pool_top;
+            E.cc_valid = false;  // union-find is refreshed by the next full batch
+            finish_time();
+            return DLP_OK;
+        }
+        bool full_cc = nd > 0 || !E.cc_valid;
+        int mode = cfg->mode;
+        long long max_iter = cfg->max_iterations > 0 ? cfg->max_iterations
+                                                      : std::max<long long>(1, 10 * E.num_alive);
+        if (kind == KIND_DYNLP) {
+            resolve_tau_dev(E, cfg->tau);
+            E.intra_k = 0;
+            if (cfg->component_init && k > 0) {
+                intra_components_dev(E, bd, base);
+                init_components_dev(E, bd, base);
+            }
+            reach_and_pin_dev(E, full_cc, n);
+            for (int c = 0; c < E.ncol; c++) lp_loop_dev(E, c, cfg->delta, max_iter, mode);
+        } else {  // ItLP: no reachability, active = alive & unlabeled & deg > 0
+            itlp_active_dev(E, n);
+            for (int c = 0; c < E.ncol; c++) itlp_dev(E, c, cfg->delta, max_iter);
+            E.cc_valid = false;
+        }
+        DLP_CUDA_TRY(cudaGetLastError());
+        E.h_ctl.reserve(E.ncol);
+        DLP_CUDA_TRY(cudaMemcpyAsync(E.h_ds.p, E.ds, sizeof(DevState), cudaMemcpyDeviceToHost, E.st));
+        DLP_CUDA_TRY(cudaMemcpyAsync(E.h_ctl.p, E.ctl, E.ncol * sizeof(LPCtl), cudaMemcpyDeviceToHost, E.st));
+        DLP_CUDA_TRY(cudaStreamSynchronize(E.st));
+        DevState& s = *E.h_ds.p;
+        E.live_edges = s.log_n;
+        E.pool_top_host = (long long)s.pool_top;
+        E.last_tau = s.tau;
+        if (kind == KIND_DYNLP) E.cc_valid = true;
+        if (E.pool_top_host > E.pool_cap) return fail(E, DLP_EINTERNAL, "adjacency pool overflow");
+        for (int c = 0; c < E.ncol; c++) {
+            LPCtl& L = E.h_ctl.p[c];
+            dlp_report& r = reps[c];
+            r.iterations = L.iterations;
+            r.updates = L.updates;
+            r.max_change = L.max_change;
+            r.converged = (int)L.converged;
+            r.isolated_pinned = s.isolated;
+            r.unreachable_pinned = kind == KIND_DYNLP ? s.unreach : 0;
+            r.warnings = L.warnings + r.isolated_pinned + r.unreachable_pinned;
+            r.edges_traversed = L.edges;
+            r.certify_sweeps = L.certs;
+            float ms = 0.f;
+            DLP_CUDA_TRY(cudaEventElapsedTime(&ms, E.lp_ev[2 * c], E.lp_ev[2 * c + 1]));
+            r.lp_kernel_ms = ms;
+            r.gpu_launches = E.launches - launches0;
+        }
+        finish_time();
+        return DLP_OK;
+    } catch (const CudaFailure& f) {
+        return cuda_fail(h, f);
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+int dlp_create(const dlp_config* cfg, int device, dlp_engine** out) {
+    *out = nullptr;
+    auto* h = new dlp_engine();
+    Engine& E = h->E;
+    try {
+        int ndev = 0;
+        DLP_CUDA_TRY(cudaGetDeviceCount(&ndev));
+        if (device < 0 || device >= ndev) {
+            delete h;
+            return DLP_ECUDA;
+        }
+        E.device = device;
+        DLP_CUDA_TRY(cudaSetDevice(device));
+        cudaDeviceProp prop;
+        DLP_CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+        E.sm_count = prop.multiProcessorCount;
+        if (!prop.cooperativeLaunch) {
+            delete h;
+            return DLP_ECUDA;
+        }
+        E.num_classes = cfg && cfg->num_classes > 2 ? cfg->num_classes : 2;
+        E.ncol = E.num_classes > 2 ? E.num_classes : 1;
+        DLP_CUDA_TRY(cudaStreamCreateWithFlags(&E.st, cudaStreamNonBlocking));
+        DLP_CUDA_TRY(cudaMalloc(&E.ds, sizeof(DevState)));
+        DLP_CUDA_TRY(cudaMemset(E.ds, 0, sizeof(DevState)));
+        DLP_CUDA_TRY(cudaMalloc(&E.ctl, E.ncol * sizeof(LPCtl)));
+        DLP_CUDA_TRY(cudaMemset(E.ctl, 0, E.ncol * sizeof(LPCtl)));
+        E.h_ds.reserve(1);
+        E.h_ctl.reserve(E.ncol);
+        ensure_vertex_capacity(E, 4096);
+        ensure_log(E, 4096);
+        compact_pool(E, 1 << 16);
+        lp_setup(E);
+        DLP_CUDA_TRY(cudaStreamSynchronize(E.st));
+    } catch (const CudaFailure& f) {
+        fprintf(stderr, "dlp_create: CUDA error %s (%s)\n", cudaGetErrorString(f.err), f.expr);
+        delete h;
+        return DLP_ECUDA;
+    }
+    *out = h;
+    return DLP_OK;
+}
+
+int dlp_destroy(dlp_engine* h) {
+    if (!h) return DLP_OK;
+    Engine& E = h->E;
+    cudaSetDevice(E.device);
+    cudaStreamSynchronize(E.st);
+    DevArray<unsigned char>* u8s[] = {&E.alive, &E.mark, &E.root_gt, &E.elig, &E.d_stage, &E.cub_tmp};
+    for (auto* a : u8s) a->release();
+    E.purge_flag.release();
+    E.gt.release();
+    E.row_start.release();
+    DevArray<int>* i32s[] = {&E.row_len, &E.row_up, &E.row_cap, &E.parent, &E.cnt_up, &E.cnt_dn, &E.grp_start,
+                             &E.list[0], &E.list[1], &E.list[2], &E.f0, &E.elist, &E.purge_list, &E.touched,
+                             &E.nbr, &E.log_lo, &E.log_hi, &E.log_lo2, &E.log_hi2, &E.val_a, &E.val_b,
+                             &E.flag_i, &E.pos_i, &E.m_lo, &E.m_hi, &E.mlo_at, &E.mhi_at, &E.lpar, &E.comp,
+                             &E.comp_sorted_i, &E.root_flag, &E.root_rank};
+    for (auto* a : i32s) a->release();
+    DevArray<double>* f64s[] = {&E.f[0], &E.f[1], &E.wgt, &E.log_w, &E.log_w2, &E.m_w, &E.ew_lo, &E.ew_hi,
+                                &E.mw_at, &E.per0, &E.per1, &E.cinit, &E.tau_scratch};
+    for (auto* a : f64s) a->release();
+    for (int i = 0; i < 3; i++) E.memb[i].release();
+    E.key_a.release();
+    E.key_b.release();
+    if (E.ds) cudaFree(E.ds);
+    if (E.ctl) cudaFree(E.ctl);
+    E.h_stage.release();
+    E.h_ds.release();
+    E.h_ctl.release();
+    for (auto ev : E.lp_ev) cudaEventDestroy(ev);
+    if (E.st) cudaStreamDestroy(E.st);
+    delete h;
+    return DLP_OK;
+}
+
+const char* dlp_last_error(dlp_engine* h) { return h ? h->E.err.c_str() : "null engine"; }
+int dlp_num_columns(dlp_engine* h) { return h->E.ncol; }
+
+int dlp_apply_batch(dlp_engine* h, const dlp_config* cfg, const dlp_batch* b, dlp_report* reps) {
+    return run_batch(h, cfg, b, false, false, reps, KIND_DYNLP);
+}
+
+int dlp_apply_batch_device(dlp_engine* h, const dlp_config* cfg, const dlp_batch* b, int trusted, dlp_report* reps) {
+    return run_batch(h, cfg, b, true, trusted != 0, reps, KIND_DYNLP);
+}
+
+int dlp_apply_structure(dlp_engine* h, const dlp_batch* b) {
+    return run_batch(h, nullptr, b, false, false, nullptr, KIND_STRUCTURE);
+}
+
+int dlp_itlp_batch(dlp_engine* h, const dlp_config* cfg, const dlp_batch* b, dlp_report* reps) {
+    return run_batch(h, cfg, b, false, false, reps, KIND_ITLP);
+}
+
+int dlp_num_slots(dlp_engine* h, int64_t* n_slots, int64_t* num_alive) {
+    *n_slots = h->E.n_slots;
+    *num_alive = h->E.num_alive;
+    return DLP_OK;
+}
+
+int dlp_read_labels(dlp_engine* h, double* f, int8_t* gt, int64_t n) {
+    Engine& E = h->E;
+    if (n != E.n_slots) return fail(E, DLP_EVALIDATION, "read_labels: n=%lld but num_slots=%lld", (long long)n, E.n_slots);
+    try {
+        DLP_CUDA_TRY(cudaSetDevice(E.device));
+        if (f && n)
+            DLP_CUDA_TRY(cudaMemcpy2DAsync(f, n * sizeof(double), E.f[0].p, E.cap_n * sizeof(double), n * sizeof(double),
+                                           E.ncol, cudaMemcpyDeviceToHost, E.st));
+        if (gt && n) DLP_CUDA_TRY(cudaMemcpyAsync(gt, E.gt.p, n, cudaMemcpyDeviceToHost, E.st));
+        DLP_CUDA_TRY(cudaStreamSynchronize(E.st));
+    } catch (const CudaFailure& e) {
+        return cuda_fail(h, e);
+    }
+    if (f)
+        for (long long i = 0; i < (long long)E.ncol * n; i++) {
+            double x = f[i];
+            if (x != x) {
+                unsigned long long b;
+                memcpy(&b, &x, 8);
+                f[i] = (double)(b & 1);
+            }
+        }
+    return DLP_OK;
+}
+
+int dlp_write_labels(dlp_engine* h, const double* f, int64_t n) {
+    Engine& E = h->E;
+    if (n != E.n_slots) return fail(E, DLP_EVALIDATION, "write_labels: n mismatch");
+    try {
+        DLP_CUDA_TRY(cudaSetDevice(E.device));
+        std::vector<signed char> g(n);
+        std::vector<double> buf((size_t)E.ncol * n);
+        if (n) DLP_CUDA_TRY(cudaMemcpy(g.data(), E.gt.p, n, cudaMemcpyDeviceToHost));
+        for (int c = 0; c < E.ncol; c++)
+            for (long long v = 0; v < n; v++) {
+                double x = f[(size_t)c * n + v];
+                if (g[v] >= 0) x = box_class(E.ncol == 1 ? g[v] : (g[v] == c ? 1 : 0));
+                buf[(size_t)c * n + v] = x;
+            }
+        for (int b = 0; b < 2; b++)
+            if (n)
+                DLP_CUDA_TRY(cudaMemcpy2DAsync(E.f[b].p, E.cap_n * sizeof(double), buf.data(), n * sizeof(double),
+                                               n * sizeof(double), E.ncol, cudaMemcpyHostToDevice, E.st));
+        DLP_CUDA_TRY(cudaStreamSynchronize(E.st));
+    } catch (const CudaFailure& e) {
+        return cuda_fail(h, e);
+    }
+    return DLP_OK;
+}
+
+int dlp_read_alive(dlp_engine* h, uint8_t* alive, int64_t n) {
+    Engine& E = h->E;
+    if (n != E.n_slots) return fail(E, DLP_EVALIDATION, "read_alive: n mismatch");
+    memcpy(alive, E.h_alive.data(), n);
+    return DLP_OK;
+}
+
+int dlp_read_eligible(dlp_engine* h, uint8_t* elig, int64_t n) {
+    Engine& E = h->E;
+    if (n != E.n_slots) return fail(E, DLP_EVALIDATION, "read_eligible: n mismatch");
+    try {
+        if (n) DLP_CUDA_TRY(cudaMemcpy(elig, E.elig.p, n, cudaMemcpyDeviceToHost));
+    } catch (const CudaFailure& e) {
+        return cuda_fail(h, e);
+    }
+    return DLP_OK;
+}
+
+int dlp_graph_stats(dlp_engine* h, int64_t* live_edges, double* last_tau) {
+    *live_edges = h->E.live_edges;
+    *last_tau = h->E.last_tau;
+    return DLP_OK;
+}
+
+int dlp_read_csr(dlp_engine* h, int64_t* indptr, int64_t* indices, double* weights, double* degrees, int64_t n,
+                 int64_t nnz) {
+    Engine& E = h->E;
+    if (n != E.n_slots || nnz != 2 * E.live_edges) return fail(E, DLP_EVALIDATION, "read_csr: size mismatch");
+    try {
+        read_csr_dev(E, (long long*)indptr, (long long*)indices, weights, degrees);
+    } catch (const CudaFailure& e) {
+        return cuda_fail(h, e);
+    }
+    return DLP_OK;
+}
+
+int dlp_read_live_edges(dlp_engine* h, int64_t* u, int64_t* v, double* w, int64_t m) {
+    Engine& E = h->E;
+    if (m != E.live_edges) return fail(E, DLP_EVALIDATION, "read_live_edges: size mismatch");
+    try {
+        std::vector<int> a(m), b(m);
+        if (m) {
+            DLP_CUDA_TRY(cudaMemcpy(a.data(), E.log_lo.p, m * sizeof(int), cudaMemcpyDeviceToHost));
+            DLP_CUDA_TRY(cudaMemcpy(b.data(), E.log_hi.p, m * sizeof(int), cudaMemcpyDeviceToHost));
+            DLP_CUDA_TRY(cudaMemcpy(w, E.log_w.p, m * sizeof(double), cudaMemcpyDeviceToHost));
+        }
+        for (long long i = 0; i < m; i++) {
+            u[i] = a[i];
+            v[i] = b[i];
+        }
+    } catch (const CudaFailure& e) {
+        return cuda_fail(h, e);
+    }
+    return DLP_OK;
+}
+
+int dlp_read_intra(dlp_engine* h, int64_t* vertices, int64_t* parent, int64_t* comp, int64_t cap, int64_t* kout) {
+    Engine& E = h->E;
+    long long k = E.intra_k;
+    *kout = k;
+    if (cap < k) return fail(E, DLP_EVALIDATION, "read_intra: capacity too small");
+    try {
+        std::vector<int> p(k), c(k);
+        if (k) {
+            DLP_CUDA_TRY(cudaMemcpy(p.data(), E.lpar.p, k * sizeof(int), cudaMemcpyDeviceToHost));
+            DLP_CUDA_TRY(cudaMemcpy(c.data(), E.comp.p, k * sizeof(int), cudaMemcpyDeviceToHost));
+        }
+        long long base = E.n_slots - k;
+        for (long long i = 0; i < k; i++) {
+            vertices[i] = base + i;
+            parent[i] = base + p[i];
+            comp[i] = c[i];
+        }
+    } catch (const CudaFailure& e) {
+        return cuda_fail(h, e);
+    }
+    return DLP_OK;
+}
+
+int dlp_device_info(int device, int* sm_count, int* cc_major, int* cc_minor) {
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return DLP_ECUDA;
+    *sm_count = prop.multiProcessorCount;
+    *cc_major = prop.major;
+    *cc_minor = prop.minor;
+    return DLP_OK;
+}
+
+}  // extern "C"

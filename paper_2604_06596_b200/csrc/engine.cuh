@@ -1,0 +1,194 @@
+// engine.cuh -- device-resident state of one DynLP engine and the launchers
+// of its per-batch pipeline.
+//
+// HBM layout (one engine per GPU):
+//   per vertex (cap_n slots):   alive u8, gt i8, row_start i64, row_len/up/cap
+//                               i32, parent i32 (global union-find),
+//                               root_gt u8, mark u8, cnt_up/cnt_dn/grp i32
+//   per label column c:         f[0][c*cap_n + v], f[1][...] fp64 (Jacobi
+//                               double buffer, GT vertices NaN-boxed),
+//                               elig[c*cap_n + v] u8
+//   adjacency pool:             nbr i32[pool_cap], w f64[pool_cap]; row v
+//                               = [up entries (y > v, insertion order) ++
+//                               down entries (y < v, insertion order)] at
+//                               row_start[v], capacity row_cap[v] (slack for
+//                               up-appends; relocation by bump allocation)
+//   edge log:                   lo/hi i32, w f64 -- live edges in insertion
+//                               order (the reference's chunk list), input of
+//                               the tau pairwise sum
+//   frontier machinery:         3 rotating id lists + 3 rotating bitmaps
+#pragma once
+
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "../../include/dynlp_b200.h"
+
+namespace dlp {
+
+// Device-side scalars that live across batches.
+struct DevState {
+    unsigned long long pool_top;  // bump allocator into the adjacency pool
+    long long log_n;              // live edge-log length
+    long long m_kept;             // merged edges appended by this batch
+    long long n_purge;            // rows to purge after deletes
+    long long n_touched;          // rows touched by inserts
+    long long n_f0;               // initial frontier size
+    long long n_elist;            // eligible list size
+    long long isolated;           // unreachable & deg 0
+    long long unreach;            // unreachable & deg > 0
+    long long intra_nc;           // intra-batch component count
+    double tau;
+    long long log_n_before;
+};
+
+// Control block of the persistent LP loop (one per column launch).
+struct LPCtl {
+    unsigned int bar;
+    unsigned int cnt[4];
+    unsigned long long rmax[3];
+    unsigned long long swept[3];
+    long long warnings;
+    long long edges;
+    // outputs
+    long long iterations;
+    long long updates;
+    double max_change;
+    long long converged;
+    long long certs;
+};
+
+template <typename T>
+struct DevArray {
+    T* p = nullptr;
+    size_t n = 0;
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    // grow to at least `want` elements, preserving the first `keep` elements
+    void reserve(size_t want, size_t keep, cudaStream_t st) {
+        if (want <= n) return;
+        size_t nn = n ? n : 1024;
+        while (nn < want) nn += nn / 2 + 1024;
+        T* q = nullptr;
+        DLP_CUDA_TRY(cudaMalloc(&q, nn * sizeof(T)));
+        if (p && keep) DLP_CUDA_TRY(cudaMemcpyAsync(q, p, keep * sizeof(T), cudaMemcpyDeviceToDevice, st));
+        if (p) {
+            DLP_CUDA_TRY(cudaStreamSynchronize(st));
+            cudaFree(p);
+        }
+        p = q;
+        n = nn;
+    }
+};
+
+template <typename T>
+struct PinnedArray {
+    T* p = nullptr;
+    size_t n = 0;
+    void reserve(size_t want) {
+        if (want <= n) return;
+        if (p) cudaFreeHost(p);
+        size_t nn = want + want / 2 + 1024;
+        DLP_CUDA_TRY(cudaMallocHost(&p, nn * sizeof(T)));
+        n = nn;
+    }
+    void release() {
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        n = 0;
+    }
+};
+
+struct BatchDev {  // device copies of one batch
+    const long long* ids;
+    const signed char* gt;
+    const long long* owner;
+    const long long* other;
+    const double* w;
+    const long long* dels;
+    long long k, ne, nd;
+};
+
+struct Engine {
+    int device = 0;
+    cudaStream_t st = nullptr;
+    int sm_count = 148;
+    int num_classes = 2;
+    int ncol = 1;
+    std::string err;
+
+    // host mirror (validation) -----------------------------------------
+    std::vector<unsigned char> h_alive;
+    long long n_slots = 0, num_alive = 0;
+    long long live_edges = 0;  // host copy of log_n after the last batch
+    long long cap_n = 0;
+    double last_tau = 0.0;
+    long long intra_k = 0;
+    bool cc_valid = true;  // global union-find consistent with the live graph
+
+    // per-vertex ----------------------------------------------------------
+    DevArray<unsigned char> alive, mark, root_gt;
+    DevArray<int> purge_flag;
+    DevArray<signed char> gt;
+    DevArray<long long> row_start;
+    DevArray<int> row_len, row_up, row_cap, parent, cnt_up, cnt_dn, grp_start;
+    DevArray<double> f[2];
+    DevArray<unsigned char> elig;
+    DevArray<unsigned int> memb[3];
+    DevArray<int> list[3], f0, elist, purge_list, touched;
+    // adjacency pool ------------------------------------------------------
+    DevArray<int> nbr;
+    DevArray<double> wgt;
+    long long pool_cap = 0, pool_top_host = 0;
+    // edge log ------------------------------------------------------------
+    DevArray<int> log_lo, log_hi, log_lo2, log_hi2;
+    DevArray<double> log_w, log_w2;
+    // batch staging -------------------------------------------------------
+    PinnedArray<unsigned char> h_stage;
+    DevArray<unsigned char> d_stage;
+    // per-batch scratch -----------------------------------------------------
+    DevArray<unsigned long long> key_a, key_b;
+    DevArray<int> val_a, val_b, flag_i, pos_i;
+    DevArray<int> m_lo, m_hi;
+    DevArray<double> m_w, ew_lo, ew_hi;  // merged edges (first-occurrence order)
+    DevArray<int> mlo_at, mhi_at;
+    DevArray<double> mw_at;
+    DevArray<int> lpar, comp, comp_sorted_i, root_flag, root_rank;
+    DevArray<double> per0, per1, cinit;
+    DevArray<unsigned char> cub_tmp;
+    DevArray<double> tau_scratch;
+    DevState* ds = nullptr;
+    PinnedArray<DevState> h_ds;
+    LPCtl* ctl = nullptr;  // [ncol]
+    PinnedArray<LPCtl> h_ctl;
+    int lp_grid = 0;
+    // instrumentation: kernel launches issued and LP kernel time per column
+    long long launches = 0;
+    std::vector<cudaEvent_t> lp_ev;  // 2 per column
+    std::vector<double> lp_ms;
+};
+
+// graph.cu ------------------------------------------------------------------
+void ensure_vertex_capacity(Engine& E, long long want);
+void ensure_pool(Engine& E, long long new_edges, long long new_vertices);
+void ensure_log(Engine& E, long long want);
+void apply_deletes_dev(Engine& E, const BatchDev& b);
+void apply_inserts_dev(Engine& E, const BatchDev& b, long long base);
+void resolve_tau_dev(Engine& E, double cfg_tau);
+void intra_components_dev(Engine& E, const BatchDev& b, long long base);
+void init_components_dev(Engine& E, const BatchDev& b, long long base);
+void reach_and_pin_dev(Engine& E, bool full_rebuild, long long n);
+void compact_pool(Engine& E, long long min_free);
+// lp.cu ---------------------------------------------------------------------
+void lp_loop_dev(Engine& E, int col, double delta, long long max_iter, int mode);
+void itlp_dev(Engine& E, int col, double delta, long long max_iter);
+void lp_setup(Engine& E);
+void itlp_active_dev(Engine& E, long long n);
+// readers (graph.cu) ----------------------------------------------------------
+void read_csr_dev(Engine& E, long long* indptr, long long* indices, double* weights, double* degrees);
+
+}  // namespace dlp

@@ -1,0 +1,200 @@
+"""GPU parity: the CUDA engine (through the C-ABI) against the reference's
+golden fixtures and the CPU oracle.  Every comparison is bitwise: f bytes,
+IterationReport fields, tau, eligible masks, CSR snapshots, intra-batch
+component labelings."""
+
+import numpy as np
+import pytest
+
+from golden_io import (STREAM_CASES, csr_digest, kernel_case, load_case, report_tuple)
+from oracle import OracleEngine
+from paper_2604_06596_b200 import streams
+from paper_2604_06596_b200.batch import BatchUpdate
+from paper_2604_06596_b200.errors import ValidationError
+
+pytestmark = pytest.mark.gpu
+
+JACOBI_CASES = [c for c in STREAM_CASES if c != "er_gauss_seidel"]
+
+
+def _engine(num_classes=2):
+    from paper_2604_06596_b200.engine import DynamicGraph, LabelState
+
+    return DynamicGraph(0, num_classes=num_classes), LabelState()
+
+
+def _cfg(case_or_kw):
+    from paper_2604_06596_b200.engine import EngineConfig
+
+    if isinstance(case_or_kw, dict):
+        return EngineConfig(**case_or_kw)
+    c = case_or_kw
+    return EngineConfig(delta=c.delta, tau=c.tau, max_iterations=c.max_iterations,
+                        component_init=c.component_init, mode=c.mode)
+
+
+def _reports(rep):
+    return rep if isinstance(rep, list) else [rep]
+
+
+@pytest.mark.parametrize("name", JACOBI_CASES)
+def test_engine_matches_reference_golden(gpu_device, name):
+    from paper_2604_06596_b200.engine import apply_batch
+
+    case = load_case(name)
+    g, lab = _engine(case.num_classes)
+    cfg = _cfg(case)
+    for t, b in enumerate(case.batches):
+        lab, rep = apply_batch(g, lab, b, cfg)
+        F = lab.F
+        assert F.shape == case.f[t].shape, (name, t)
+        assert F.tobytes() == case.f[t].tobytes(), f"{name} batch {t}: f differs " \
+            f"(max abs {np.abs(F - case.f[t]).max():.3g})"
+        for c, r in enumerate(_reports(rep)):
+            assert report_tuple(r) == tuple(case.rep_i[t, c]), f"{name} batch {t} col {c}"
+            assert r.max_change == case.rep_mc[t, c]
+        if not b.is_empty:
+            if case.tau == "auto":
+                assert g.last_tau == case.tau_vals[t], f"{name} batch {t}: tau"
+            assert np.array_equal(g.eligible(), case.elig[t]), f"{name} batch {t}: eligible"
+            csr = g.csr()
+            assert csr_digest(csr.indptr, csr.indices, csr.weights, csr.degrees) == case.csr_sha[t], \
+                f"{name} batch {t}: CSR"
+            if case.component_init and len(b.insert_ids):
+                v, p, c = g.intra_labeling()
+                assert np.array_equal(np.stack([v, p, c]), case.intra[t]), f"{name} batch {t}: intra"
+    g.close()
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_kernel_plugin_matches_reference_golden(gpu_device, seed):
+    from paper_2604_06596_b200 import kernels as K
+
+    k = kernel_case(seed)
+    vals = np.empty(len(k["frontier"]))
+    deltas = np.empty(len(k["frontier"]))
+    K.jacobi_step(k["indptr"], k["indices"], k["weights"], k["gt"], k["f"], k["frontier"], vals,
+                  deltas, 1)
+    assert vals.tobytes() == k["vals"].tobytes()
+    assert deltas.tobytes() == k["deltas"].tobytes()
+    f = k["f"].copy()
+    elig = k["elig"].copy()
+    max_iters = 10_000 if seed != 0 else 5
+    it, upd, mc, warn, left = K.jacobi_run(k["indptr"], k["indices"], k["weights"], k["gt"], f,
+                                           k["frontier"], elig, 1e-7, max_iters, 1)
+    assert [it, upd, warn, len(left)] == list(k["run_out"])
+    assert mc == k["run_mc"][0]
+    assert f.tobytes() == k["run_f"].tobytes()
+    assert np.array_equal(elig, k["run_elig"])
+    assert np.array_equal(left, k["run_left"])
+    f3 = k["f"].copy()
+    d3 = np.empty(len(k["frontier"]))
+    K.gauss_seidel_step(k["indptr"], k["indices"], k["weights"], k["gt"], f3, k["frontier"], d3)
+    assert f3.tobytes() == k["gs_f"].tobytes()
+    assert d3.tobytes() == k["gs_deltas"].tobytes()
+
+
+def _compare_with_oracle(batches, num_classes=2, **kw):
+    from paper_2604_06596_b200.engine import apply_batch
+
+    g, lab = _engine(num_classes)
+    cfg = _cfg(dict(kw))
+    orc = OracleEngine(num_classes, threads=4)
+    for t, b in enumerate(batches):
+        lab, rep = apply_batch(g, lab, b, cfg)
+        oreps = orc.apply_batch(b, **kw)
+        for r, o in zip(_reports(rep), oreps):
+            assert report_tuple(r) == report_tuple(o), f"batch {t}"
+            assert r.max_change == o.max_change, f"batch {t}"
+            assert r.edges_traversed == o.edges_traversed, f"batch {t}"
+        F = lab.F
+        of, _ = orc.labels()
+        assert F.tobytes() == of.tobytes(), f"batch {t}: max abs {np.abs(F - of).max():.3g}"
+    tau = orc.last_tau
+    g.close()
+    return tau
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_engine_vs_oracle_mixed_blob_stream(gpu_device, seed):
+    bl = streams.make_blobs(6000, 16, 2, seed)
+    e = streams.knn_graph_exact(bl.x, 10)
+    gt = streams.stratified_seeds(bl.classes, 0.01, seed)
+    s = streams.phased_stream(6000, e, bl.classes, gt, 600, seed, 0.69, 0.01, 0.30, initial_gt=4)
+    _compare_with_oracle(s.batches, delta=1e-5)
+
+
+def test_engine_vs_oracle_ten_class_columns(gpu_device):
+    bl = streams.make_blobs(4000, 32, 10, 7)
+    e = streams.knn_graph_exact(bl.x, 10)
+    gt = streams.stratified_seeds(bl.classes, 0.01, 7)
+    s = streams.phased_stream(4000, e, bl.classes, gt, 500, 7, 0.99, 0.01, 0.0, initial_gt=20)
+    _compare_with_oracle(s.batches, num_classes=10, delta=1e-4)
+
+
+def test_engine_vs_oracle_er_heavy_deletes_explicit_tau(gpu_device):
+    n = 5000
+    e = streams.erdos_renyi_edges(n, 8, 3)
+    classes = np.random.default_rng(3).integers(0, 2, n).astype(np.int8)
+    gt = streams.stratified_seeds(classes, 0.02, 3)
+    s = streams.phased_stream(n, e, classes, gt, 400, 3, 0.6, 0.02, 0.38, initial_gt=4)
+    _compare_with_oracle(s.batches, delta=1e-6, tau=0.55)
+
+
+def test_engine_budget_and_noinit_vs_oracle(gpu_device):
+    bl = streams.make_blobs(3000, 8, 2, 11)
+    e = streams.knn_graph_exact(bl.x, 6)
+    gt = streams.stratified_seeds(bl.classes, 0.02, 11)
+    s = streams.phased_stream(3000, e, bl.classes, gt, 300, 11, 0.8, 0.02, 0.18, initial_gt=4)
+    _compare_with_oracle(s.batches, delta=1e-7, max_iterations=7, component_init=False)
+
+
+def test_single_whole_graph_batch_vs_oracle(gpu_device):
+    bl = streams.make_blobs(20000, 16, 2, 5)
+    e = streams.knn_graph_exact(bl.x, 10, block=2048)
+    gt = {int(v): int(bl.classes[v]) for v in streams.stratified_seeds(bl.classes, 0.01, 5)}
+    b = streams.single_batch(20000, e, gt)
+    _compare_with_oracle([b], delta=1e-4)
+
+
+def test_validation_errors_leave_state_unchanged(gpu_device):
+    from paper_2604_06596_b200.engine import EngineConfig, apply_batch
+
+    g, lab = _engine()
+    cfg = EngineConfig(delta=1e-9)
+    pre = BatchUpdate.from_records([(0, [], 0), (1, [(1, 0, 1.0)], None), (2, [(2, 1, 1.0)], 1)])
+    apply_batch(g, lab, pre, cfg)
+    before = lab.f.copy()
+    bad = [
+        (BatchUpdate.from_records([(3, [(3, 9, 1.0)], None)], deletes=[1]), "edge to unknown vertex 9"),
+        (BatchUpdate.from_records(deletes=[1, 1]), "duplicate vertex id in deletes"),
+        (BatchUpdate.from_records(deletes=[7]), "unknown vertex id 7 in deletes"),
+        (BatchUpdate.from_records([(4, [], None)]), "insert ids must be the contiguous block 3..3"),
+        (BatchUpdate.from_records([(3, [(3, 0, -1.0)], None)]), "negative weight on edge to vertex 0"),
+        (BatchUpdate.from_records([(3, [(3, 1, 1.0)], None)], deletes=[1]),
+         "edge to vertex 1 deleted in the same batch"),
+        (BatchUpdate.from_records([(3, [], 2)]), "ground-truth class must be 0 or 1"),
+    ]
+    for batch, msg in bad:
+        with pytest.raises(ValidationError, match=msg):
+            apply_batch(g, lab, batch, cfg)
+    assert g.num_slots == 3 and g.num_alive == 3 and g.edge_count == 2
+    assert np.array_equal(lab.f, before)
+    g.close()
+
+
+def test_bitwise_repeatable(gpu_device):
+    from paper_2604_06596_b200.engine import EngineConfig, apply_batch
+
+    bl = streams.make_blobs(5000, 16, 2, 21)
+    e = streams.knn_graph_exact(bl.x, 10)
+    gt = streams.stratified_seeds(bl.classes, 0.01, 21)
+    s = streams.phased_stream(5000, e, bl.classes, gt, 1000, 21, 0.9, 0.01, 0.09, initial_gt=4)
+    blobs = set()
+    for _ in range(3):
+        g, lab = _engine()
+        for b in s.batches:
+            apply_batch(g, lab, b, EngineConfig(delta=1e-6))
+        blobs.add(lab.f.tobytes())
+        g.close()
+    assert len(blobs) == 1
