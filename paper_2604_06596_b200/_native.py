@@ -12,7 +12,7 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libdynlp_b200.so")
+LIB_PATH = os.environ.get("DLP_LIB_PATH") or os.path.join(HERE, "libdynlp_b200.so")
 
 
 class Batch(C.Structure):

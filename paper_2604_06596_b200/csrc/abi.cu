@@ -398,7 +398,7 @@ int dlp_destroy(dlp_engine* h) {
                              &E.list[0], &E.list[1], &E.list[2], &E.f0, &E.elist, &E.purge_list, &E.touched,
                              &E.nbr, &E.log_lo, &E.log_hi, &E.log_lo2, &E.log_hi2, &E.val_a, &E.val_b,
                              &E.flag_i, &E.pos_i, &E.m_lo, &E.m_hi, &E.mlo_at, &E.mhi_at, &E.lpar, &E.comp,
-                             &E.comp_sorted_i, &E.root_flag, &E.root_rank};
+                             &E.comp_sorted_i, &E.root_flag, &E.root_rank, &E.root_tmp};
     for (auto* a : i32s) a->release();
     DevArray<double>* f64s[] = {&E.f[0], &E.f[1], &E.wgt, &E.log_w, &E.log_w2, &E.m_w, &E.ew_lo, &E.ew_hi,
                                 &E.mw_at, &E.per0, &E.per1, &E.cinit, &E.tau_scratch};

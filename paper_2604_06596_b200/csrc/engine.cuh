@@ -157,7 +157,7 @@ struct Engine {
     DevArray<double> m_w, ew_lo, ew_hi;  // merged edges (first-occurrence order)
     DevArray<int> mlo_at, mhi_at;
     DevArray<double> mw_at;
-    DevArray<int> lpar, comp, comp_sorted_i, root_flag, root_rank;
+    DevArray<int> lpar, comp, comp_sorted_i, root_flag, root_rank, root_tmp;
     DevArray<double> per0, per1, cinit;
     DevArray<unsigned char> cub_tmp;
     DevArray<double> tau_scratch;

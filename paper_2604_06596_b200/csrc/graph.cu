@@ -117,6 +117,15 @@ __device__ inline int uf_find(int* par, int x) {
     return cur;
 }
 
+// Root without path compression.  Flatten passes must not compress: a
+// concurrent compression store could overwrite a slot that another thread
+// has just set to its final root with a non-root ancestor.
+__device__ inline int uf_root(const int* par, int x) {
+    int cur = x, next;
+    while ((next = par[cur]) != cur) cur = next;
+    return cur;
+}
+
 __device__ inline void uf_unite(int* par, int a, int b) {
     int ra = uf_find(par, a), rb = uf_find(par, b);
     while (ra != rb) {
@@ -777,11 +786,16 @@ __global__ void k_intra_union(const long long* ids, const long long* owner, cons
     }
 }
 
-__global__ void k_intra_flatten(int* lpar, long long k, int* root_flag) {
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < k; i += (long long)gridDim.x * blockDim.x) {
-        int r = uf_find(lpar, (int)i);
-        lpar[i] = r;
-        root_flag[i] = (r == i) ? 1 : 0;
+__global__ void k_roots(const int* par, long long n, int* root) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        root[i] = uf_root(par, (int)i);
+}
+
+__global__ void k_adopt_roots(int* par, const int* root, long long n, int* root_flag) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        int r = root[i];
+        par[i] = r;
+        if (root_flag) root_flag[i] = (r == i) ? 1 : 0;
     }
 }
 
@@ -812,7 +826,10 @@ void intra_components_dev(Engine& E, const BatchDev& b, long long base) {
     E.launches++;
     if (b.ne) k_intra_union<<<grid_for(b.ne), kBlock, 0, st>>>(b.ids, b.owner, b.other, b.w, b.ne, base, k, E.ds, E.lpar.p);
     E.launches++;
-    k_intra_flatten<<<grid_for(k), kBlock, 0, st>>>(E.lpar.p, k, E.root_flag.p);
+    E.root_tmp.reserve(std::max<long long>(k, E.cap_n) + 1, 0, st);
+    k_roots<<<grid_for(k), kBlock, 0, st>>>(E.lpar.p, k, E.root_tmp.p);
+    E.launches++;
+    k_adopt_roots<<<grid_for(k), kBlock, 0, st>>>(E.lpar.p, E.root_tmp.p, k, E.root_flag.p);
     E.launches++;
     cub_scan(E, E.root_flag.p, E.root_rank.p, k);
     k_intra_comp<<<grid_for(k), kBlock, 0, st>>>(E.lpar.p, E.root_rank.p, E.root_flag.p, k, E.comp.p, E.key_a.p,
@@ -929,15 +946,10 @@ __global__ void k_uf_union_merged(const int* lo, const int* hi, const DevState* 
 __global__ void k_uf_flatten_root_gt(int* par, long long n, const unsigned char* alive, const signed char* gt,
                                      unsigned char* root_gt) {
     for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < n; v += (long long)gridDim.x * blockDim.x) {
-        int r = uf_find(par, (int)v);
-        if (alive[v] && gt[v] >= 0) root_gt[r] = 1;
+        if (alive[v] && gt[v] >= 0) root_gt[par[v]] = 1;
     }
 }
 
-__global__ void k_uf_flatten(int* par, long long n) {
-    for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < n; v += (long long)gridDim.x * blockDim.x)
-        par[v] = uf_find(par, (int)v);
-}
 
 __global__ void k_eligible(long long n, int ncol, long long cap, const unsigned char* alive, const signed char* gt,
                            const int* par, const unsigned char* root_gt, const int* row_len, unsigned char* mark,
@@ -985,7 +997,10 @@ void reach_and_pin_dev(Engine& E, bool full_rebuild, long long n) {
         E.launches++;
     }
     DLP_CUDA_TRY(cudaMemsetAsync(E.root_gt.p, 0, n, st));
-    k_uf_flatten<<<grid_for(n), kBlock, 0, st>>>(E.parent.p, n);
+    E.root_tmp.reserve(E.cap_n + 1, 0, st);
+    k_roots<<<grid_for(n), kBlock, 0, st>>>(E.parent.p, n, E.root_tmp.p);
+    E.launches++;
+    k_adopt_roots<<<grid_for(n), kBlock, 0, st>>>(E.parent.p, E.root_tmp.p, n, nullptr);
     E.launches++;
     k_uf_flatten_root_gt<<<grid_for(n), kBlock, 0, st>>>(E.parent.p, n, E.alive.p, E.gt.p, E.root_gt.p);
     E.launches++;

@@ -20,6 +20,7 @@
 // append); per-round scalars rotate through small arrays so no reset races a
 // reader.
 #include <cooperative_groups.h>
+#include <cstdlib>
 
 #include "engine.cuh"
 
@@ -64,18 +65,24 @@ __device__ inline void claim(unsigned int* M, int* L, unsigned int* cnt, int v) 
     L[base + g.thread_rank()] = v;
 }
 
+#ifdef DLP_LP_CG
+#define LDX(p) __ldcg(p)
+#else
+#define LDX(p) (*(p))
+#endif
+
 // _update_one over the engine's row layout; X holds boxed labels.
 __device__ inline double eval_row(const LPParams& P, const double* X, int u, long long* s_out, int* len_out,
                                   double* val) {
     long long s = P.row_start[u];
     int len = P.row_len[u];
-    double fu = X[u];
+    double fu = LDX(X + u);
     RowAcc acc;
     acc.init();
     for (int e = 0; e < len; e++) {
         int v = P.nbr[s + e];
         double we = P.w[s + e];
-        double x = X[v];
+        double x = LDX(X + v);
         acc.add(we, is_boxed(x) ? boxed_class(x) : -1, x, fu);
     }
     *s_out = s;
@@ -128,7 +135,7 @@ __device__ void lp_round(const LPParams& P, const int* cur, long long ncur, cons
     double lmax = 0.0;
     long long ledges = 0, lswept = 0, lwarn = 0;
     for (long long i = tid; i < ncur; i += nth) {
-        int u = cur[i];
+        int u = LDX(cur + i);
         if (certify && !P.elig[u]) continue;
         lswept++;
         long long s;
@@ -152,8 +159,8 @@ __device__ void lp_round(const LPParams& P, const int* cur, long long ncur, cons
         }
     }
     for (long long i = tid; i < nprev; i += nth) {
-        int u = prev[i];
-        if (!test_bit(Mc, u)) Y[u] = X[u];
+        int u = LDX(prev + i);
+        if (!((LDX(Mc + (u >> 5)) >> (u & 31)) & 1u)) Y[u] = LDX(X + u);
         clear_bit(Mp, u);
     }
     block_flush(lmax, ledges, lswept, lwarn, rmax_slot, swept_slot, P.ctl);
@@ -268,6 +275,7 @@ void lp_setup(Engine& E) {
     if (occ < 1) occ = 1;
     if (occ > 8) occ = 8;
     E.lp_grid = E.sm_count * occ;
+    if (const char* g = getenv("DLP_LP_GRID")) E.lp_grid = atoi(g);
 }
 
 void lp_loop_dev(Engine& E, int col, double delta, long long max_iter, int mode) {
