@@ -377,10 +377,18 @@ def main():
     # ---- aggregates -------------------------------------------------------------
     upd = sum(r.updates for step in repsA for r in step)
     edges = sum(r.edges_traversed for step in repsA for r in step)
-    lp_ms = sum(r.lp_kernel_ms for step in repsA for r in step)
-    launches = sum(step[-1].gpu_launches for step in repsA) / K
-    alg_bytes = 32.0 * upd + 21.0 * edges
+    lp_ms = sum(step[0].lp_kernel_ms for step in repsA)  # one fused launch per step
+    launches = sum(step[0].gpu_launches for step in repsA) / K
+    rounds = sum(step[0].lp_rounds for step in repsA) / K
+    urows = sum(step[0].lp_union_rows for step in repsA)
+    uent = sum(step[0].lp_union_entries for step in repsA)
+    # algorithmic bytes of the fused kernel: per union row
+    # 16 B row bounds + 4 B emask; per gathered entry 4 B id + 8 B weight + 8*C B
+    # label vector; per (vertex, column) update 8 B f read + 8 B staged write +
+    # 8 B staged read + 8 B commit write.
+    alg_bytes = 20.0 * urows + (12.0 + 8.0 * ncol) * uent + 32.0 * upd
     achieved = alg_bytes / (lp_ms * 1e-3) / 1e9 if lp_ms > 0 else None
+    survey_bytes = 32.0 * upd + 21.0 * edges  # SURVEY §8(d) D-4 per-column model
     peak, peak_kind = measured_peaks()
     tr = traffic_record()
     same = all(a[c].iterations == b[c].iterations and a[c].updates == b[c].updates
@@ -396,11 +404,15 @@ def main():
         "edges_per_s": edges / (ms_value * K * 1e-3),
         "vertex_updates_per_batch": upd / K, "edge_relaxations_per_batch": edges / K,
         "lp_kernel_share": lp_ms / (ms_value * K),
+        "lp_rounds_per_batch": rounds, "lp_union_rows_per_batch": urows / K,
+        "lp_union_entries_per_batch": uent / K,
+        "survey_model_gbs": survey_bytes / (lp_ms * 1e-3) / 1e9 if lp_ms > 0 else None,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None,
                      "traffic": (tr or {}).get("dram_bytes_per_alg_byte"),
                      "kernel": "k_lp_loop (persistent frontier/certify loop)",
-                     "algorithmic_bytes": "32 B/vertex-update + 21 B/edge-entry (SURVEY §8(d) D-4)",
+                     "algorithmic_bytes": "fused kernel: 20 B/union row + (12 + 8C) B/gathered entry + "
+                                          "32 B/(vertex, column) update; see DESIGN.md",
                      "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})"},
         "e2e": {"value": ms_e2e, "unit": "ms/batch", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h)},

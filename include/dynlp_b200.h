@@ -75,8 +75,11 @@ typedef struct {
     double wall_time_ms;
     int64_t edges_traversed; /* sum of row lengths over every vertex update */
     int64_t certify_sweeps;
-    double lp_kernel_ms;     /* CUDA-event time of this column's propagation kernel */
-    int64_t gpu_launches;    /* kernels this call launched so far (all columns) */
+    double lp_kernel_ms;     /* CUDA-event time of the batch's fused propagation kernel */
+    int64_t gpu_launches;    /* kernels this call launched (all columns) */
+    int64_t lp_rounds;       /* lockstep rounds of the fused kernel (all columns) */
+    int64_t lp_union_rows;   /* rows the fused kernel evaluated (once for all columns) */
+    int64_t lp_union_entries;/* row entries it gathered (one C-wide gather each) */
 } dlp_report;
 
 /* Engine lifetime: replaces DynamicGraph() + LabelState() (graph.py:179,
@@ -89,7 +92,7 @@ int dlp_num_columns(dlp_engine* e);
 /* engine.apply_batch (engine.py:328-413) with HOST batch arrays.  Writes one
  * report per label column (1 for binary).  cfg may differ between calls
  * (delta / tau / max_iterations / component_init / mode); num_classes is
- * fixed at dlp_create. */
+ * fixed at dlp_create (at most 16 label columns). */
 int dlp_apply_batch(dlp_engine* e, const dlp_config* cfg, const dlp_batch* batch,
                     dlp_report* reports);
 /* Same, batch arrays already resident in device memory (bench "value" leg).

@@ -40,7 +40,8 @@ class Report(C.Structure):
         ("warnings", C.c_int64), ("isolated_pinned", C.c_int64),
         ("unreachable_pinned", C.c_int64), ("wall_time_ms", C.c_double),
         ("edges_traversed", C.c_int64), ("certify_sweeps", C.c_int64),
-        ("lp_kernel_ms", C.c_double), ("gpu_launches", C.c_int64),
+        ("lp_kernel_ms", C.c_double), ("gpu_launches", C.c_int64), ("lp_rounds", C.c_int64),
+        ("lp_union_rows", C.c_int64), ("lp_union_entries", C.c_int64),
     ]
 
 

@@ -285,7 +285,6 @@ int run_batch(dlp_engine* h, const dlp_config* cfg, const dlp_batch* batch, bool
             return DLP_OK;
         }
         bool full_cc = nd > 0 || !E.cc_valid;
-        int mode = cfg->mode;
         long long max_iter = cfg->max_iterations > 0 ? cfg->max_iterations
                                                       : std::max<long long>(1, 10 * E.num_alive);
         if (kind == KIND_DYNLP) {
@@ -296,16 +295,15 @@ int run_batch(dlp_engine* h, const dlp_config* cfg, const dlp_batch* batch, bool
                 init_components_dev(E, bd, base);
             }
             reach_and_pin_dev(E, full_cc, n);
-            for (int c = 0; c < E.ncol; c++) lp_loop_dev(E, c, cfg->delta, max_iter, mode);
+            lp_run_dev(E, cfg->delta, max_iter, false);
         } else {  // ItLP: no reachability, active = alive & unlabeled & deg > 0
             itlp_active_dev(E, n);
-            for (int c = 0; c < E.ncol; c++) itlp_dev(E, c, cfg->delta, max_iter);
+            lp_run_dev(E, cfg->delta, max_iter, true);
             E.cc_valid = false;
         }
         DLP_CUDA_TRY(cudaGetLastError());
-        E.h_ctl.reserve(E.ncol);
         DLP_CUDA_TRY(cudaMemcpyAsync(E.h_ds.p, E.ds, sizeof(DevState), cudaMemcpyDeviceToHost, E.st));
-        DLP_CUDA_TRY(cudaMemcpyAsync(E.h_ctl.p, E.ctl, E.ncol * sizeof(LPCtl), cudaMemcpyDeviceToHost, E.st));
+        DLP_CUDA_TRY(cudaMemcpyAsync(E.h_ctl.p, E.ctl, sizeof(LPCtl), cudaMemcpyDeviceToHost, E.st));
         DLP_CUDA_TRY(cudaStreamSynchronize(E.st));
         DevState& s = *E.h_ds.p;
         E.live_edges = s.log_n;
@@ -313,22 +311,25 @@ int run_batch(dlp_engine* h, const dlp_config* cfg, const dlp_batch* batch, bool
         E.last_tau = s.tau;
         if (kind == KIND_DYNLP) E.cc_valid = true;
         if (E.pool_top_host > E.pool_cap) return fail(E, DLP_EINTERNAL, "adjacency pool overflow");
+        float lp_ms = 0.f;
+        DLP_CUDA_TRY(cudaEventElapsedTime(&lp_ms, E.lp_ev[0], E.lp_ev[1]));
+        const LPCtl& L = *E.h_ctl.p;
         for (int c = 0; c < E.ncol; c++) {
-            LPCtl& L = E.h_ctl.p[c];
             dlp_report& r = reps[c];
-            r.iterations = L.iterations;
-            r.updates = L.updates;
-            r.max_change = L.max_change;
-            r.converged = (int)L.converged;
+            r.iterations = L.iterations[c];
+            r.updates = L.updates[c];
+            r.max_change = L.max_change[c];
+            r.converged = (int)L.converged[c];
             r.isolated_pinned = s.isolated;
             r.unreachable_pinned = kind == KIND_DYNLP ? s.unreach : 0;
-            r.warnings = L.warnings + r.isolated_pinned + r.unreachable_pinned;
-            r.edges_traversed = L.edges;
-            r.certify_sweeps = L.certs;
-            float ms = 0.f;
-            DLP_CUDA_TRY(cudaEventElapsedTime(&ms, E.lp_ev[2 * c], E.lp_ev[2 * c + 1]));
-            r.lp_kernel_ms = ms;
+            r.warnings = L.warnings[c] + r.isolated_pinned + r.unreachable_pinned;
+            r.edges_traversed = L.edges[c];
+            r.certify_sweeps = L.certs[c];
+            r.lp_kernel_ms = lp_ms;  // one fused launch serves every column
             r.gpu_launches = E.launches - launches0;
+            r.lp_rounds = L.rounds;
+            r.lp_union_rows = L.urows;
+            r.lp_union_entries = L.uentries;
         }
         finish_time();
         return DLP_OK;
@@ -366,10 +367,14 @@ int dlp_create(const dlp_config* cfg, int device, dlp_engine** out) {
         DLP_CUDA_TRY(cudaStreamCreateWithFlags(&E.st, cudaStreamNonBlocking));
         DLP_CUDA_TRY(cudaMalloc(&E.ds, sizeof(DevState)));
         DLP_CUDA_TRY(cudaMemset(E.ds, 0, sizeof(DevState)));
-        DLP_CUDA_TRY(cudaMalloc(&E.ctl, E.ncol * sizeof(LPCtl)));
-        DLP_CUDA_TRY(cudaMemset(E.ctl, 0, E.ncol * sizeof(LPCtl)));
+        if (E.ncol > kMaxCols) {
+            delete h;
+            return DLP_EVALIDATION;
+        }
+        DLP_CUDA_TRY(cudaMalloc(&E.ctl, sizeof(LPCtl)));
+        DLP_CUDA_TRY(cudaMemset(E.ctl, 0, sizeof(LPCtl)));
         E.h_ds.reserve(1);
-        E.h_ctl.reserve(E.ncol);
+        E.h_ctl.reserve(1);
         ensure_vertex_capacity(E, 4096);
         ensure_log(E, 4096);
         compact_pool(E, 1 << 16);
@@ -389,13 +394,13 @@ int dlp_destroy(dlp_engine* h) {
     Engine& E = h->E;
     cudaSetDevice(E.device);
     cudaStreamSynchronize(E.st);
-    DevArray<unsigned char>* u8s[] = {&E.alive, &E.mark, &E.root_gt, &E.elig, &E.d_stage, &E.cub_tmp};
+    DevArray<unsigned char>* u8s[] = {&E.alive, &E.mark, &E.root_gt, &E.d_stage, &E.cub_tmp};
     for (auto* a : u8s) a->release();
     E.purge_flag.release();
     E.gt.release();
     E.row_start.release();
     DevArray<int>* i32s[] = {&E.row_len, &E.row_up, &E.row_cap, &E.parent, &E.cnt_up, &E.cnt_dn, &E.grp_start,
-                             &E.list[0], &E.list[1], &E.list[2], &E.f0, &E.elist, &E.purge_list, &E.touched,
+                             &E.ulist[0], &E.ulist[1], &E.f0, &E.elist, &E.purge_list, &E.touched,
                              &E.nbr, &E.log_lo, &E.log_hi, &E.log_lo2, &E.log_hi2, &E.val_a, &E.val_b,
                              &E.flag_i, &E.pos_i, &E.m_lo, &E.m_hi, &E.mlo_at, &E.mhi_at, &E.lpar, &E.comp,
                              &E.comp_sorted_i, &E.root_flag, &E.root_rank, &E.root_tmp};
@@ -403,7 +408,8 @@ int dlp_destroy(dlp_engine* h) {
     DevArray<double>* f64s[] = {&E.f[0], &E.f[1], &E.wgt, &E.log_w, &E.log_w2, &E.m_w, &E.ew_lo, &E.ew_hi,
                                 &E.mw_at, &E.per0, &E.per1, &E.cinit, &E.tau_scratch};
     for (auto* a : f64s) a->release();
-    for (int i = 0; i < 3; i++) E.memb[i].release();
+    DevArray<unsigned int>* u32s[] = {&E.eligm, &E.emask_store, &E.fmask[0], &E.fmask[1]};
+    for (auto* x : u32s) x->release();
     E.key_a.release();
     E.key_b.release();
     if (E.ds) cudaFree(E.ds);
@@ -411,7 +417,8 @@ int dlp_destroy(dlp_engine* h) {
     E.h_stage.release();
     E.h_ds.release();
     E.h_ctl.release();
-    for (auto ev : E.lp_ev) cudaEventDestroy(ev);
+    for (auto ev : E.lp_ev)
+        if (ev) cudaEventDestroy(ev);
     if (E.st) cudaStreamDestroy(E.st);
     delete h;
     return DLP_OK;
@@ -447,11 +454,21 @@ int dlp_read_labels(dlp_engine* h, double* f, int8_t* gt, int64_t n) {
     if (n != E.n_slots) return fail(E, DLP_EVALIDATION, "read_labels: n=%lld but num_slots=%lld", (long long)n, E.n_slots);
     try {
         DLP_CUDA_TRY(cudaSetDevice(E.device));
-        if (f && n)
-            DLP_CUDA_TRY(cudaMemcpy2DAsync(f, n * sizeof(double), E.f[0].p, E.cap_n * sizeof(double), n * sizeof(double),
-                                           E.ncol, cudaMemcpyDeviceToHost, E.st));
+        std::vector<double> buf;
+        if (f && n) {
+            if (E.ncol == 1) {
+                DLP_CUDA_TRY(cudaMemcpyAsync(f, E.f[0].p, n * sizeof(double), cudaMemcpyDeviceToHost, E.st));
+            } else {
+                buf.resize((size_t)n * E.ncol);
+                DLP_CUDA_TRY(cudaMemcpyAsync(buf.data(), E.f[0].p, buf.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                                             E.st));
+            }
+        }
         if (gt && n) DLP_CUDA_TRY(cudaMemcpyAsync(gt, E.gt.p, n, cudaMemcpyDeviceToHost, E.st));
         DLP_CUDA_TRY(cudaStreamSynchronize(E.st));
+        if (f && E.ncol > 1)
+            for (long long v = 0; v < n; v++)
+                for (int c = 0; c < E.ncol; c++) f[(size_t)c * n + v] = buf[(size_t)v * E.ncol + c];
     } catch (const CudaFailure& e) {
         return cuda_fail(h, e);
     }
@@ -479,12 +496,12 @@ int dlp_write_labels(dlp_engine* h, const double* f, int64_t n) {
             for (long long v = 0; v < n; v++) {
                 double x = f[(size_t)c * n + v];
                 if (g[v] >= 0) x = box_class(E.ncol == 1 ? g[v] : (g[v] == c ? 1 : 0));
-                buf[(size_t)c * n + v] = x;
+                buf[(size_t)v * E.ncol + c] = x;
             }
         for (int b = 0; b < 2; b++)
             if (n)
-                DLP_CUDA_TRY(cudaMemcpy2DAsync(E.f[b].p, E.cap_n * sizeof(double), buf.data(), n * sizeof(double),
-                                               n * sizeof(double), E.ncol, cudaMemcpyHostToDevice, E.st));
+                DLP_CUDA_TRY(cudaMemcpyAsync(E.f[b].p, buf.data(), buf.size() * sizeof(double), cudaMemcpyHostToDevice,
+                                             E.st));
         DLP_CUDA_TRY(cudaStreamSynchronize(E.st));
     } catch (const CudaFailure& e) {
         return cuda_fail(h, e);
@@ -503,7 +520,9 @@ int dlp_read_eligible(dlp_engine* h, uint8_t* elig, int64_t n) {
     Engine& E = h->E;
     if (n != E.n_slots) return fail(E, DLP_EVALIDATION, "read_eligible: n mismatch");
     try {
-        if (n) DLP_CUDA_TRY(cudaMemcpy(elig, E.elig.p, n, cudaMemcpyDeviceToHost));
+        std::vector<unsigned int> m(n);
+        if (n) DLP_CUDA_TRY(cudaMemcpy(m.data(), E.eligm.p, n * sizeof(unsigned int), cudaMemcpyDeviceToHost));
+        for (long long v = 0; v < n; v++) elig[v] = m[v] != 0;
     } catch (const CudaFailure& e) {
         return cuda_fail(h, e);
     }

@@ -5,9 +5,11 @@
 //   per vertex (cap_n slots):   alive u8, gt i8, row_start i64, row_len/up/cap
 //                               i32, parent i32 (global union-find),
 //                               root_gt u8, mark u8, cnt_up/cnt_dn/grp i32
-//   per label column c:         f[0][c*cap_n + v], f[1][...] fp64 (Jacobi
-//                               double buffer, GT vertices NaN-boxed),
-//                               elig[c*cap_n + v] u8
+//   labels:                     f[0][v*C + c] fp64, C = label columns
+//                               interleaved per vertex (one gather serves
+//                               every column; GT vertices NaN-boxed);
+//                               f[1] = staging buffer of the Jacobi round;
+//                               eligm[v] u32 = eligible columns bitmask
 //   adjacency pool:             nbr i32[pool_cap], w f64[pool_cap]; row v
 //                               = [up entries (y > v, insertion order) ++
 //                               down entries (y < v, insertion order)] at
@@ -16,7 +18,8 @@
 //   edge log:                   lo/hi i32, w f64 -- live edges in insertion
 //                               order (the reference's chunk list), input of
 //                               the tau pairwise sum
-//   frontier machinery:         3 rotating id lists + 3 rotating bitmaps
+//   frontier machinery:         union frontier lists + per-vertex column
+//                               masks (2 rotating each)
 #pragma once
 
 #include <string>
@@ -43,20 +46,39 @@ struct DevState {
     long long log_n_before;
 };
 
-// Control block of the persistent LP loop (one per column launch).
+constexpr int kMaxCols = 16;  // label columns handled by the fused LP kernel
+
+// Per-round results of the fused LP kernel (two rotating slots).
+struct RoundSlot {
+    unsigned long long rmax[kMaxCols];   // max |delta| per column (IEEE bits)
+    unsigned long long neval[kMaxCols];  // vertex updates per column
+    unsigned long long edges[kMaxCols];  // row entries traversed per column
+    unsigned long long warn[kMaxCols];   // isolated sentinels per column
+    unsigned long long urows;            // union rows evaluated (all columns at once)
+    unsigned long long uentries;         // row entries gathered for them
+    unsigned int claimed;                // columns with a non-empty next frontier
+    unsigned int grab;                   // dynamic chunk counter of this round
+    unsigned int cnt;                    // length of the union frontier being built
+    unsigned int pad;
+};
+
+// Control block of the persistent LP kernel (one launch per batch, all columns).
 struct LPCtl {
     unsigned int bar;
-    unsigned int cnt[4];
-    unsigned long long rmax[3];
-    unsigned long long swept[3];
-    long long warnings;
-    long long edges;
-    // outputs
-    long long iterations;
-    long long updates;
-    double max_change;
-    long long converged;
-    long long certs;
+    unsigned int pad;
+    RoundSlot slot[2];
+    long long elig_count[kMaxCols];
+    // outputs per column
+    long long iterations[kMaxCols];
+    long long updates[kMaxCols];
+    long long certs[kMaxCols];
+    long long warnings[kMaxCols];
+    long long edges[kMaxCols];
+    double max_change[kMaxCols];
+    long long converged[kMaxCols];
+    long long rounds;  // global (lockstep) rounds executed
+    long long urows;
+    long long uentries;
 };
 
 template <typename T>
@@ -137,9 +159,8 @@ struct Engine {
     DevArray<long long> row_start;
     DevArray<int> row_len, row_up, row_cap, parent, cnt_up, cnt_dn, grp_start;
     DevArray<double> f[2];
-    DevArray<unsigned char> elig;
-    DevArray<unsigned int> memb[3];
-    DevArray<int> list[3], f0, elist, purge_list, touched;
+    DevArray<unsigned int> eligm, emask_store, fmask[2];
+    DevArray<int> ulist[2], f0, elist, purge_list, touched;
     // adjacency pool ------------------------------------------------------
     DevArray<int> nbr;
     DevArray<double> wgt;
@@ -163,13 +184,13 @@ struct Engine {
     DevArray<double> tau_scratch;
     DevState* ds = nullptr;
     PinnedArray<DevState> h_ds;
-    LPCtl* ctl = nullptr;  // [ncol]
+    LPCtl* ctl = nullptr;
     PinnedArray<LPCtl> h_ctl;
     int lp_grid = 0;
+    size_t lp_smem = 0;
     // instrumentation: kernel launches issued and LP kernel time per column
     long long launches = 0;
-    std::vector<cudaEvent_t> lp_ev;  // 2 per column
-    std::vector<double> lp_ms;
+    cudaEvent_t lp_ev[2] = {nullptr, nullptr};
 };
 
 // graph.cu ------------------------------------------------------------------
@@ -184,8 +205,7 @@ void init_components_dev(Engine& E, const BatchDev& b, long long base);
 void reach_and_pin_dev(Engine& E, bool full_rebuild, long long n);
 void compact_pool(Engine& E, long long min_free);
 // lp.cu ---------------------------------------------------------------------
-void lp_loop_dev(Engine& E, int col, double delta, long long max_iter, int mode);
-void itlp_dev(Engine& E, int col, double delta, long long max_iter);
+void lp_run_dev(Engine& E, double delta, long long max_iter, bool itlp);
 void lp_setup(Engine& E);
 void itlp_active_dev(Engine& E, long long n);
 // readers (graph.cu) ----------------------------------------------------------

@@ -39,24 +39,6 @@ static void grow_zero(DevArray<T>& a, size_t want, size_t keep, cudaStream_t st)
     (void)old;
 }
 
-// Column-major per-column arrays are re-laid out on growth (stride = cap_n).
-template <typename T>
-static void grow_columns(DevArray<T>& a, int ncol, long long old_cap, long long new_cap, long long used,
-                         cudaStream_t st) {
-    T* q = nullptr;
-    DLP_CUDA_TRY(cudaMalloc(&q, (size_t)ncol * new_cap * sizeof(T)));
-    DLP_CUDA_TRY(cudaMemsetAsync(q, 0, (size_t)ncol * new_cap * sizeof(T), st));
-    if (a.p && used)
-        DLP_CUDA_TRY(cudaMemcpy2DAsync(q, new_cap * sizeof(T), a.p, old_cap * sizeof(T), used * sizeof(T), ncol,
-                                       cudaMemcpyDeviceToDevice, st));
-    if (a.p) {
-        DLP_CUDA_TRY(cudaStreamSynchronize(st));
-        cudaFree(a.p);
-    }
-    a.p = q;
-    a.n = (size_t)ncol * new_cap;
-}
-
 void ensure_vertex_capacity(Engine& E, long long want) {
     if (want <= E.cap_n) return;
     long long nc = E.cap_n ? E.cap_n : 4096;
@@ -76,17 +58,18 @@ void ensure_vertex_capacity(Engine& E, long long want) {
     grow_zero(E.cnt_dn, nc, keep, st);
     grow_zero(E.grp_start, nc, 0, st);
     grow_zero(E.purge_flag, nc, keep, st);
-    for (int i = 0; i < 3; i++) {
-        grow_zero(E.memb[i], (nc + 31) / 32 + 1, (keep + 31) / 32 + 1, st);
-        E.list[i].reserve(nc + 1, 0, st);
+    for (int i = 0; i < 2; i++) {
+        grow_zero(E.fmask[i], nc, keep, st);
+        E.ulist[i].reserve(nc + 1, 0, st);
     }
+    grow_zero(E.eligm, nc, keep, st);
+    grow_zero(E.emask_store, nc, keep, st);
     E.f0.reserve(nc + 1, 0, st);
     E.elist.reserve(nc + 1, 0, st);
     E.purge_list.reserve(nc + 1, 0, st);
     E.touched.reserve(nc + 1, 0, st);
-    grow_columns(E.f[0], E.ncol, E.cap_n, nc, keep, st);
-    grow_columns(E.f[1], E.ncol, E.cap_n, nc, keep, st);
-    grow_columns(E.elig, E.ncol, E.cap_n, nc, keep, st);
+    grow_zero(E.f[0], (size_t)nc * E.ncol, (size_t)keep * E.ncol, st);
+    grow_zero(E.f[1], (size_t)nc * E.ncol, (size_t)keep * E.ncol, st);
     E.cap_n = nc;
 }
 
@@ -305,8 +288,8 @@ __global__ void k_grow(const long long* ids, const signed char* gtin, long long 
                 x = box_class(g);
             else
                 x = box_class(g == c ? 1 : 0);
-            f0[c * cap + v] = x;
-            f1[c * cap + v] = x;
+            f0[v * ncol + c] = x;
+            f1[v * ncol + c] = x;
         }
         mark[v] = 1;
         row_start[v] = 0;
@@ -903,8 +886,8 @@ __global__ void k_comp_assign(long long base, long long k, int ncol, long long c
         long long v = base + i;
         if (gt[v] != -1) continue;
         double x = cinit[c * k + comp[i]];
-        f0[c * cap + v] = x;
-        f1[c * cap + v] = x;
+        f0[v * ncol + c] = x;
+        f1[v * ncol + c] = x;
     }
 }
 
@@ -953,17 +936,18 @@ __global__ void k_uf_flatten_root_gt(int* par, long long n, const unsigned char*
 
 __global__ void k_eligible(long long n, int ncol, long long cap, const unsigned char* alive, const signed char* gt,
                            const int* par, const unsigned char* root_gt, const int* row_len, unsigned char* mark,
-                           unsigned char* elig, double* f0, double* f1, int* elist, int* f0list, DevState* ds) {
+                           unsigned int* eligm, double* f0, double* f1, int* elist, int* f0list, DevState* ds) {
+    unsigned int allc = ncol >= 32 ? 0xffffffffu : ((1u << ncol) - 1u);
     long long iso = 0, unr = 0;
     for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < n; v += (long long)gridDim.x * blockDim.x) {
         bool unl = alive[v] && gt[v] == -1;
         bool reached = alive[v] && root_gt[par[v]];
         bool e = unl && reached;
-        for (int c = 0; c < ncol; c++) elig[c * cap + v] = e ? 1 : 0;
+        eligm[v] = e ? allc : 0u;
         if (unl && !reached) {
             for (int c = 0; c < ncol; c++) {
-                f0[c * cap + v] = 0.5;
-                f1[c * cap + v] = 0.5;
+                f0[v * ncol + c] = 0.5;
+                f1[v * ncol + c] = 0.5;
             }
             if (row_len[v] == 0)
                 iso++;
@@ -1005,7 +989,7 @@ void reach_and_pin_dev(Engine& E, bool full_rebuild, long long n) {
     k_uf_flatten_root_gt<<<grid_for(n), kBlock, 0, st>>>(E.parent.p, n, E.alive.p, E.gt.p, E.root_gt.p);
     E.launches++;
     k_eligible<<<grid_for(n), kBlock, 0, st>>>(n, E.ncol, E.cap_n, E.alive.p, E.gt.p, E.parent.p, E.root_gt.p,
-                                               E.row_len.p, E.mark.p, E.elig.p, E.f[0].p, E.f[1].p, E.elist.p, E.f0.p,
+                                               E.row_len.p, E.mark.p, E.eligm.p, E.f[0].p, E.f[1].p, E.elist.p, E.f0.p,
                                                E.ds);
     E.launches++;
 }

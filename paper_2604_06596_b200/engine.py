@@ -92,6 +92,9 @@ class IterationReport:
     certify_sweeps: int = 0
     lp_kernel_ms: float = 0.0
     gpu_launches: int = 0
+    lp_rounds: int = 0
+    lp_union_rows: int = 0
+    lp_union_entries: int = 0
 
     def to_json_dict(self) -> dict:
         return {k: getattr(self, k) for k in (
@@ -301,7 +304,9 @@ def _reports(reps, method):
                             unreachable_pinned=r.unreachable_pinned,
                             wall_time_ms=r.wall_time_ms, edges_traversed=r.edges_traversed,
                             certify_sweeps=r.certify_sweeps, lp_kernel_ms=r.lp_kernel_ms,
-                            gpu_launches=r.gpu_launches) for r in reps]
+                            gpu_launches=r.gpu_launches, lp_rounds=r.lp_rounds,
+                            lp_union_rows=r.lp_union_rows, lp_union_entries=r.lp_union_entries)
+            for r in reps]
 
 
 class LabelState:
