@@ -417,6 +417,10 @@ def main():
         "e2e": {"value": ms_e2e, "unit": "ms/batch", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h)},
         "gpu_launches": launches, "clocks": clk,
+        "step_wall_ms": {"value": [round(r[0].wall_time_ms, 2) for r in repsA],
+                         "e2e": [round(r[0].wall_time_ms, 2) for r in repsB],
+                         "lp_kernel": [round(r[0].lp_kernel_ms, 2) for r in repsA]},
+        "certify_sweeps_per_batch": sum(r.certify_sweeps for step in repsA for r in step) / K,
         "legs_identical_work": same,
     }
     if rank == 0 and not args.no_cpu_baseline:

@@ -314,6 +314,7 @@ int run_batch(dlp_engine* h, const dlp_config* cfg, const dlp_batch* batch, bool
         float lp_ms = 0.f;
         DLP_CUDA_TRY(cudaEventElapsedTime(&lp_ms, E.lp_ev[0], E.lp_ev[1]));
         const LPCtl& L = *E.h_ctl.p;
+        lp_dump_trace(E, L.rounds);
         for (int c = 0; c < E.ncol; c++) {
             dlp_report& r = reps[c];
             r.iterations = L.iterations[c];
@@ -400,7 +401,7 @@ int dlp_destroy(dlp_engine* h) {
     E.gt.release();
     E.row_start.release();
     DevArray<int>* i32s[] = {&E.row_len, &E.row_up, &E.row_cap, &E.parent, &E.cnt_up, &E.cnt_dn, &E.grp_start,
-                             &E.ulist[0], &E.ulist[1], &E.f0, &E.elist, &E.purge_list, &E.touched,
+                             &E.ulist[0], &E.ulist[1], &E.llist[0], &E.llist[1], &E.hlist[0], &E.hlist[1], &E.elist_s, &E.elist_l, &E.elist_h, &E.f0, &E.elist, &E.purge_list, &E.touched,
                              &E.nbr, &E.log_lo, &E.log_hi, &E.log_lo2, &E.log_hi2, &E.val_a, &E.val_b,
                              &E.flag_i, &E.pos_i, &E.m_lo, &E.m_hi, &E.mlo_at, &E.mhi_at, &E.lpar, &E.comp,
                              &E.comp_sorted_i, &E.root_flag, &E.root_rank, &E.root_tmp};

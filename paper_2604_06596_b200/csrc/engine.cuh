@@ -57,9 +57,8 @@ struct RoundSlot {
     unsigned long long urows;            // union rows evaluated (all columns at once)
     unsigned long long uentries;         // row entries gathered for them
     unsigned int claimed;                // columns with a non-empty next frontier
-    unsigned int grab;                   // dynamic chunk counter of this round
-    unsigned int cnt;                    // length of the union frontier being built
-    unsigned int pad;
+    unsigned int grab[3];                // dynamic work counters per row class (short / long / hub)
+    unsigned int cnt[3];                 // lengths of the next union frontier lists per class
 };
 
 // Control block of the persistent LP kernel (one launch per batch, all columns).
@@ -68,6 +67,8 @@ struct LPCtl {
     unsigned int pad;
     RoundSlot slot[2];
     long long elig_count[kMaxCols];
+    unsigned int n_el[3];  // eligible list split by row class (short / long / hub)
+    unsigned int n_f0[3];  // initial frontier split
     // outputs per column
     long long iterations[kMaxCols];
     long long updates[kMaxCols];
@@ -79,6 +80,11 @@ struct LPCtl {
     long long rounds;  // global (lockstep) rounds executed
     long long urows;
     long long uentries;
+    // optional per-round trace (DLP_LP_TRACE): {nS, nL, fr|ce<<16, globaltimer}
+    unsigned long long* trace;
+    long long trace_cap;
+    int* seen;               // debug: per-vertex round stamp (duplicate work items)
+    unsigned long long dups; // debug: duplicate work items detected
 };
 
 template <typename T>
@@ -160,7 +166,7 @@ struct Engine {
     DevArray<int> row_len, row_up, row_cap, parent, cnt_up, cnt_dn, grp_start;
     DevArray<double> f[2];
     DevArray<unsigned int> eligm, emask_store, fmask[2];
-    DevArray<int> ulist[2], f0, elist, purge_list, touched;
+    DevArray<int> ulist[2], llist[2], hlist[2], elist_s, elist_l, elist_h, f0, elist, purge_list, touched;
     // adjacency pool ------------------------------------------------------
     DevArray<int> nbr;
     DevArray<double> wgt;
@@ -187,6 +193,9 @@ struct Engine {
     LPCtl* ctl = nullptr;
     PinnedArray<LPCtl> h_ctl;
     int lp_grid = 0;
+    DevArray<unsigned long long> lp_trace;
+    DevArray<int> lp_seen;
+    const char* lp_trace_path = nullptr;
     size_t lp_smem = 0;
     // instrumentation: kernel launches issued and LP kernel time per column
     long long launches = 0;
@@ -207,6 +216,7 @@ void compact_pool(Engine& E, long long min_free);
 // lp.cu ---------------------------------------------------------------------
 void lp_run_dev(Engine& E, double delta, long long max_iter, bool itlp);
 void lp_setup(Engine& E);
+void lp_dump_trace(Engine& E, long long rounds);
 void itlp_active_dev(Engine& E, long long n);
 // readers (graph.cu) ----------------------------------------------------------
 void read_csr_dev(Engine& E, long long* indptr, long long* indices, double* weights, double* degrees);

@@ -61,7 +61,12 @@ void ensure_vertex_capacity(Engine& E, long long want) {
     for (int i = 0; i < 2; i++) {
         grow_zero(E.fmask[i], nc, keep, st);
         E.ulist[i].reserve(nc + 1, 0, st);
+        E.llist[i].reserve(nc + 1, 0, st);
+        E.hlist[i].reserve(nc + 1, 0, st);
     }
+    E.elist_s.reserve(nc + 1, 0, st);
+    E.elist_l.reserve(nc + 1, 0, st);
+    E.elist_h.reserve(nc + 1, 0, st);
     grow_zero(E.eligm, nc, keep, st);
     grow_zero(E.emask_store, nc, keep, st);
     E.f0.reserve(nc + 1, 0, st);

@@ -20,18 +20,29 @@
 //   the union of the columns' frontiers (or the eligible list when a column
 //   certifies); every row is read ONCE per round for all columns and one
 //   gather of X[v*C .. v*C+C) serves every column.
-// * CTA tiles.  A block grabs a chunk of up to 32 rows (dynamic atomic
-//   scheduling), gathers the chunk's row entries entry-parallel into shared
-//   memory (coalesced row reads, independent gathers), then one thread per
-//   (row, column) accumulates the row in stored order -- the reference's
-//   sequential fp64 summation -- from shared memory.  Rows of any length
-//   (kNN hubs reach thousands of entries) are streamed window by window, so
-//   load balance no longer depends on the degree distribution.
-// * Jacobi commit: phase 1 writes new values to the staging buffer Y, phase 2
-//   copies them into X; two grid-wide barriers per round.
+// * Two row classes.  Short rows (<= kLongRow entries, the bulk of a kNN
+//   graph) are evaluated warp-independently: a warp grabs 32/C rows, lane
+//   (row, column) walks its row in stored order -- the reference's sequential
+//   fp64 summation -- with kUnroll entries in flight (independent id/weight
+//   loads, then independent label gathers, then the ordered sums).  No CTA
+//   barrier is involved, so warps overlap each other's memory latency.
+//   Long rows (kNN hubs reach thousands of entries) are evaluated by a whole
+//   CTA: window by window the CTA gathers the entries and precomputes the
+//   independent product terms (f[v]-fu)*w in parallel into shared memory,
+//   then one thread per column runs the ordered dependent sums.
+// * Cache policy.  Adjacency (ids, weights) and the compact staging buffer
+//   are streamed (evict-first); label reads and commits carry an L2
+//   evict_last policy so the C-wide label vectors stay L2-resident while the
+//   adjacency streams through.
+// * Jacobi commit: phase 1 writes new values to a compact staging buffer
+//   (indexed by work item), phase 2 copies them into X; two grid-wide
+//   barriers per round.
 #include <cooperative_groups.h>
 
+#include <algorithm>
+#include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 #include "engine.cuh"
 
@@ -40,10 +51,21 @@ namespace cg = cooperative_groups;
 namespace dlp {
 
 constexpr int kLpThreads = 256;
-constexpr int kChunkRows = 32;
-constexpr int kWin = 512;  // row entries staged per window
+constexpr int kWin = 64;        // row entries per warp window
+constexpr int kHubWin = 256;    // row entries per CTA window (hub rows)
+constexpr int kLongRow = 96;    // rows longer than this are warp tiles of their own
+constexpr int kHubRow = 1024;   // rows longer than this are evaluated by a whole CTA
+constexpr int kScanRatio = 64;  // rounds with >= n/64 rows expand by atomicOr + compaction
 
 enum { PH_FRONTIER = 0, PH_DONE = 2 };
+enum { CLS_SHORT = 0, CLS_LONG = 1, CLS_HUB = 2 };
+
+// row-class thresholds (kLongRow / kHubRow by default; DLP_LONG_ROW / DLP_HUB_ROW override)
+__constant__ int c_long_row = kLongRow;
+__constant__ int c_hub_row = kHubRow;
+__device__ inline int row_class(int len) {
+    return len > c_hub_row ? CLS_HUB : (len > c_long_row ? CLS_LONG : CLS_SHORT);
+}
 
 struct LPParams {
     const long long* row_start;
@@ -51,19 +73,19 @@ struct LPParams {
     const int* nbr;
     const double* w;
     double* X;  // canonical labels [v*C + c]
-    double* Y;  // staging
+    double* Y;  // compact staging: [i*C + c] for work item i of the round
     unsigned int* eligm;
     unsigned int* emask_store;
-    unsigned int* fmask0;
-    unsigned int* fmask1;
-    int* U0;
-    int* U1;
+    unsigned int* fmask[2];
+    int* flist[3][2];  // union frontier lists per row class (rotating)
+    int* elist_c[3];   // eligible list split by row class (prologue)
     const int* f0;
     const int* elist;
     const DevState* ds;
     LPCtl* ctl;
     double delta;
     long long max_iter;
+    long long n;  // vertex slots
     int C;
     int itlp;
 };
@@ -84,26 +106,41 @@ struct ColState {
     int done;
 };
 
-__device__ inline int row_of(const int* off, int nrows, int g) {
-    int lo = 0, hi = nrows;  // largest r with off[r] <= g
-    while (hi - lo > 1) {
-        int mid = (lo + hi) >> 1;
-        if (off[mid] <= g)
-            lo = mid;
-        else
-            hi = mid;
-    }
-    return lo;
+// ---- cache-policy loads: labels stay L2-resident, adjacency streams -------
+__device__ inline unsigned long long l2_evict_last_policy() {
+    unsigned long long pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ inline double ld_keep(const double* p, unsigned long long pol) {
+    double v;
+    asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ inline void st_keep(double* p, double v, unsigned long long pol) {
+    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
+
+// warp-aggregated append: every converged caller must pass the same list/count
+__device__ inline void append_u32(int* list, unsigned int* count, int v) {
+    cg::coalesced_group g = cg::coalesced_threads();
+    unsigned int base = 0;
+    if (g.thread_rank() == 0) base = atomicAdd(count, g.size());
+    base = g.shfl(base, 0);
+    list[base + g.thread_rank()] = v;
 }
 
 struct ClaimCtx {
     unsigned int* fm_next;
-    int* U_next;
-    unsigned int* cnt;
+    int* next[3];
+    unsigned int* cnt;  // [3]
     const unsigned int* eligm;
+    const int* row_len;
     unsigned int claimed;  // per-thread OR of claimed column bits
 };
 
+// append-mode claim: add v (for the columns in `bits` where it is eligible)
+// to the next union frontier; the first claimer appends it to its class list
 __device__ inline void claim(ClaimCtx& k, int v, unsigned int bits) {
     bits &= k.eligm[v];
     if (!bits) return;
@@ -113,16 +150,19 @@ __device__ inline void claim(ClaimCtx& k, int v, unsigned int bits) {
     if ((cur & bits) == bits) return;
     unsigned int old = atomicOr(fm, bits);
     if (old != 0) return;
-    cg::coalesced_group g = cg::coalesced_threads();
-    unsigned int base = 0;
-    if (g.thread_rank() == 0) base = atomicAdd(k.cnt, g.size());
-    base = g.shfl(base, 0);
-    k.U_next[base + g.thread_rank()] = v;
+    int cls = row_class(k.row_len[v]);
+    if (cls == CLS_SHORT)
+        append_u32(k.next[0], &k.cnt[0], v);
+    else if (cls == CLS_LONG)
+        append_u32(k.next[1], &k.cnt[1], v);
+    else
+        append_u32(k.next[2], &k.cnt[2], v);
 }
 
 // Controller: every block updates its shared copy of the per-column state
 // from the finished round's slot and decides the next round's actions.
-__device__ void decide_actions(ColState& S, const LPParams& P, const RoundSlot* res, int first) {
+__device__ void decide_actions(ColState& S, const LPParams& P, const unsigned long long* res, const unsigned int* claimed,
+                               int first) {
     int C = P.C;
     unsigned int fr = 0, ce = 0;
     int done = 1;
@@ -131,12 +171,12 @@ __device__ void decide_actions(ColState& S, const LPParams& P, const RoundSlot* 
         if (!first && S.phase[c] != PH_DONE) {
             bool was_fr = (S.fr_mask & bit) != 0, was_ce = (S.cert_mask & bit) != 0;
             if (was_fr || was_ce) {
-                double rm = __longlong_as_double((long long)res->rmax[c]);
+                double rm = __longlong_as_double((long long)res[c]);
                 S.iterations[c]++;
-                S.updates[c] += (long long)res->neval[c];
-                S.edges[c] += (long long)res->edges[c];
-                S.warnings[c] += (long long)res->warn[c];
-                S.has_frontier[c] = (res->claimed & bit) != 0;
+                S.updates[c] += (long long)res[kMaxCols + c];
+                S.edges[c] += (long long)res[2 * kMaxCols + c];
+                S.warnings[c] += (long long)res[3 * kMaxCols + c];
+                S.has_frontier[c] = (*claimed & bit) != 0;
                 if (P.itlp) {
                     S.max_change[c] = rm;
                     if (rm <= P.delta) {
@@ -191,37 +231,356 @@ __device__ void decide_actions(ColState& S, const LPParams& P, const RoundSlot* 
     S.done = done;
 }
 
-__global__ void __launch_bounds__(kLpThreads) k_lp_fused(LPParams P) {
+// Per-block counters of one round (reduced into the round slot at its end).
+struct BlockCounters {
+    unsigned long long rmax[kMaxCols], neval[kMaxCols], edges[kMaxCols], warn[kMaxCols];
+    unsigned long long urows, uent;
+    unsigned int claimed;
+};
+
+// Per-warp tile descriptors (rows of the tile, their masks and offsets).
+struct WarpTile {
+    long long st[32];
+    int u[32], len[32], off[33];
+    unsigned int em[32];
+};
+
+__device__ inline int tile_row_of(const int* off, int nrows, int g) {
+    int lo = 0, hi = nrows;  // largest r with off[r] <= g
+    while (hi - lo > 1) {
+        int mid = (lo + hi) >> 1;
+        if (off[mid] <= g)
+            lo = mid;
+        else
+            hi = mid;
+    }
+    return lo;
+}
+
+// Round context shared by the tile routine.
+struct RoundCtx {
+    const int* W;           // work list of this row class
+    long long ybase;        // staging slot of W[0]
+    unsigned int FR, CE;    // column actions of the round
+    const unsigned int* fm_cur;
+    bool scan_mode;         // expand by fire-and-forget atomicOr + compaction
+};
+
+// Evaluate `nrows` consecutive work items W[k0 ..] as one warp tile:
+// entry-parallel gathers staged in warp-private shared memory (product terms
+// precomputed), then lane (row, column) runs the ordered sums; finally the
+// changed rows claim themselves and their neighbours.
+__device__ void warp_tile(const LPParams& P, const RoundCtx& R, ClaimCtx& K, BlockCounters& B, WarpTile& T,
+                          double* sw, double* sx, double* sfu, long long k0, int nrows, unsigned long long pol) {
+    const int C = P.C;
+    const int lane = threadIdx.x & 31;
+    // ---- tile rows
+    int len = 0;
+    unsigned int em = 0;
+    if (lane < nrows) {
+        int u = R.W[k0 + lane];
+        em = P.itlp ? (R.CE & P.eligm[u]) : (((R.fm_cur[u] & R.FR) | R.CE) & P.eligm[u]);
+        P.emask_store[u] = em;
+        long long st = 0;
+        if (em) {
+            st = P.row_start[u];
+            len = P.row_len[u];
+        }
+        T.u[lane] = u;
+        T.em[lane] = em;
+        T.st[lane] = st;
+        T.len[lane] = len;
+    }
+    __syncwarp();  // T.* written by lane r is read by other lanes below
+    int incl = len;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane < nrows) T.off[lane] = incl - len;
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    {
+        unsigned int nz = __ballot_sync(0xffffffffu, em != 0);
+        if (lane == 0 && nz) {
+            atomicAdd(&B.urows, (unsigned long long)__popc(nz));
+            atomicAdd(&B.uent, (unsigned long long)total);
+        }
+    }
+    for (int i = lane; i < nrows * C; i += 32) {
+        int r = i / C, c = i - r * C;
+        sfu[i] = ((T.em[r] >> c) & 1u) ? P.X[(long long)T.u[r] * C + c] : 0.0;
+    }
+    __syncwarp();
+    // ---- accumulate lanes
+    const int ar = lane / C, ac = lane - ar * C;
+    const bool aact = ar < nrows && ((T.em[ar] >> ac) & 1u);
+    RowAcc acc;
+    acc.init();
+    const int a_lo = aact ? T.off[ar] : 0, a_hi = aact ? T.off[ar] + T.len[ar] : 0;
+    for (int wb = 0; wb < total; wb += kWin) {
+        const int wn = min(kWin, total - wb);
+        // gather: kWin/32 entries per lane, all loads independent
+        int vv[kWin / 32], rr[kWin / 32];
+        double ww[kWin / 32];
+#pragma unroll
+        for (int j = 0; j < kWin / 32; j++) {
+            int i = lane + 32 * j;
+            rr[j] = -1;
+            if (i < wn) {
+                int g = wb + i;
+                int r = tile_row_of(T.off, nrows, g);
+                long long p = T.st[r] + (g - T.off[r]);
+                rr[j] = r;
+                vv[j] = __ldcs(P.nbr + p);
+                ww[j] = __ldcs(P.w + p);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < kWin / 32; j++) {
+            if (rr[j] < 0) continue;
+            int i = lane + 32 * j, r = rr[j];
+            unsigned int emr = T.em[r];
+            sw[i] = ww[j];
+            const double* xv = P.X + (long long)vv[j] * C;
+            for (int c = 0; c < C; c++) {
+                if (!((emr >> c) & 1u)) continue;
+                double x = ld_keep(xv + c, pol);
+                // product terms are independent: precompute them here, the ordered
+                // sums below keep the reference's summation order
+                sx[i * C + c] = is_boxed(x) ? x : __dmul_rn(__dsub_rn(x, sfu[r * C + c]), ww[j]);
+            }
+        }
+        __syncwarp();
+        if (aact) {
+            const int lo = max(a_lo, wb) - wb, hi = min(a_hi, wb + wn) - wb;
+            for (int t = lo; t < hi; t++) {
+                double w = sw[t], x = sx[t * C + ac];
+                acc.w_all = __dadd_rn(acc.w_all, w);
+                if (is_boxed(x)) {
+                    if (boxed_class(x) == 0)
+                        acc.w0 = __dadd_rn(acc.w0, w);
+                    else
+                        acc.w1 = __dadd_rn(acc.w1, w);
+                } else {
+                    acc.s = __dadd_rn(acc.s, x);
+                }
+            }
+        }
+        __syncwarp();
+    }
+    // ---- finish: stage, count, flag
+    unsigned int ch = 0;
+    if (aact) {
+        const int u = T.u[ar];
+        const double fu = sfu[ar * C + ac];
+        double val;
+        double d = acc.finish(fu, &val);
+        __stcs(P.Y + (R.ybase + k0 + ar) * C + ac, val);
+        atomicAdd(&B.neval[ac], 1ULL);
+        atomicAdd(&B.edges[ac], (unsigned long long)T.len[ar]);
+        if (d < 0.0) {  // isolated sentinel (_csr.pyx:49-51, 170-173)
+            atomicAdd(&B.warn[ac], 1ULL);
+            atomicAnd(&P.eligm[u], ~(1u << ac));
+            atomicAdd((unsigned long long*)&P.ctl->elig_count[ac], ~0ULL);
+        } else {
+            if (d > 0.0) atomicMax(&B.rmax[ac], dbits(d));
+            if (!P.itlp && d > P.delta) ch = 1u << ac;
+        }
+    }
+    if (P.itlp) return;
+    // ---- expand (jacobi_run commit loop, _csr.pyx:175-191)
+    const unsigned int bal = __ballot_sync(0xffffffffu, ch != 0);
+    if (!bal) return;
+    const unsigned int cmask = C >= 32 ? 0xffffffffu : ((1u << C) - 1u);
+    // lane (row, c) can only flag column c: a row's mask is its slice of the ballot
+    if (lane < nrows) {
+        unsigned int m = (bal >> (lane * C)) & cmask;
+        if (m) {
+            K.claimed |= m;  // u changed, so u itself is eligible for those columns
+            if (R.scan_mode)
+                atomicOr(&K.fm_next[T.u[lane]], m);
+            else
+                claim(K, T.u[lane], m);
+        }
+    }
+    for (int g = lane; g < total; g += 32) {
+        int r = tile_row_of(T.off, nrows, g);
+        unsigned int m = (bal >> (r * C)) & cmask;
+        if (!m) continue;
+        int v = __ldcs(P.nbr + T.st[r] + (g - T.off[r]));
+        if (R.scan_mode)
+            atomicOr(&K.fm_next[v], m);  // no return value: a fire-and-forget RED
+        else
+            claim(K, v, m);
+    }
+}
+
+// Hub row (row_len > kHubRow) evaluated by the whole CTA: windows of
+// kHubWin entries are gathered by warps 1..7 (product terms precomputed)
+// into a double buffer while warp 0 (one lane per column) runs the ordered
+// sums over the previous window.
+__device__ void cta_hub_row(const LPParams& P, const RoundCtx& R, ClaimCtx& K, BlockCounters& B, double* buf,
+                            double* s_fu, long long k, unsigned long long pol, int* s_i, long long* s_ll,
+                            unsigned int* s_u32) {
+    const int C = P.C;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    // s_i: [0] u [1] len; s_ll[0] st; s_u32: [0] em [1] chg
+    if (tid == 0) {
+        int u = R.W[k];
+        unsigned int em = P.itlp ? (R.CE & P.eligm[u]) : (((R.fm_cur[u] & R.FR) | R.CE) & P.eligm[u]);
+        P.emask_store[u] = em;
+        s_i[0] = u;
+        s_u32[0] = em;
+        s_u32[1] = 0;
+        s_i[1] = em ? P.row_len[u] : 0;
+        s_ll[0] = em ? P.row_start[u] : 0;
+        if (em) {
+            atomicAdd(&B.urows, 1ULL);
+            atomicAdd(&B.uent, (unsigned long long)s_i[1]);
+        }
+    }
+    __syncthreads();
+    const unsigned int em = s_u32[0];
+    if (!em) return;
+    const int u = s_i[0], len = s_i[1];
+    const long long st = s_ll[0];
+    if (tid < C) s_fu[tid] = ((em >> tid) & 1u) ? P.X[(long long)u * C + tid] : 0.0;
+    __syncthreads();
+    const int nwin = (len + kHubWin - 1) / kHubWin;
+    const int bsz = kHubWin * (C + 1);
+    auto gather = [&](int w, int t0, int nth) {
+        double* sw = buf + (w & 1) * bsz;
+        double* sx = sw + kHubWin;
+        const int wb = w * kHubWin, wn = min(kHubWin, len - wb);
+        for (int i = t0; i < wn; i += nth) {
+            long long p = st + wb + i;
+            int v = __ldcs(P.nbr + p);
+            double wt = __ldcs(P.w + p);
+            sw[i] = wt;
+            const double* xv = P.X + (long long)v * C;
+            for (int c = 0; c < C; c++) {
+                if (!((em >> c) & 1u)) continue;
+                double x = ld_keep(xv + c, pol);
+                sx[i * C + c] = is_boxed(x) ? x : __dmul_rn(__dsub_rn(x, s_fu[c]), wt);
+            }
+        }
+    };
+    gather(0, tid, kLpThreads);
+    __syncthreads();
+    const bool act = tid < C && ((em >> tid) & 1u);
+    RowAcc acc;
+    acc.init();
+    for (int w = 0; w < nwin; w++) {
+        if (warp != 0) {
+            if (w + 1 < nwin) gather(w + 1, tid - 32, kLpThreads - 32);
+        } else if (act) {
+            const double* sw = buf + (w & 1) * bsz;
+            const double* sx = sw + kHubWin;
+            const int wn = min(kHubWin, len - w * kHubWin);
+            for (int t = 0; t < wn; t++) {
+                double wt = sw[t], x = sx[t * C + tid];
+                acc.w_all = __dadd_rn(acc.w_all, wt);
+                if (is_boxed(x)) {
+                    if (boxed_class(x) == 0)
+                        acc.w0 = __dadd_rn(acc.w0, wt);
+                    else
+                        acc.w1 = __dadd_rn(acc.w1, wt);
+                } else {
+                    acc.s = __dadd_rn(acc.s, x);
+                }
+            }
+        }
+        __syncthreads();
+    }
+    if (act) {
+        double val;
+        double d = acc.finish(s_fu[tid], &val);
+        __stcs(P.Y + (R.ybase + k) * C + tid, val);
+        atomicAdd(&B.neval[tid], 1ULL);
+        atomicAdd(&B.edges[tid], (unsigned long long)len);
+        if (d < 0.0) {
+            atomicAdd(&B.warn[tid], 1ULL);
+            atomicAnd(&P.eligm[u], ~(1u << tid));
+            atomicAdd((unsigned long long*)&P.ctl->elig_count[tid], ~0ULL);
+        } else {
+            if (d > 0.0) atomicMax(&B.rmax[tid], dbits(d));
+            if (!P.itlp && d > P.delta) atomicOr(&s_u32[1], 1u << tid);
+        }
+    }
+    __syncthreads();
+    const unsigned int m = s_u32[1];
+    if (m) {
+        if (tid == 0) {
+            K.claimed |= m;
+            if (R.scan_mode)
+                atomicOr(&K.fm_next[u], m);
+            else
+                claim(K, u, m);
+        }
+        for (int t = tid; t < len; t += kLpThreads) {
+            int v = __ldcs(P.nbr + st + t);
+            if (R.scan_mode)
+                atomicOr(&K.fm_next[v], m);
+            else
+                claim(K, v, m);
+        }
+    }
+    (void)lane;
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(kLpThreads, 2) k_lp_fused(LPParams P) {
     extern __shared__ double smem_dyn[];
     __shared__ ColState S;
-    __shared__ int s_u[kChunkRows], s_len[kChunkRows], s_off[kChunkRows + 1];
-    __shared__ long long s_st[kChunkRows];
-    __shared__ unsigned int s_em[kChunkRows], s_chg[kChunkRows];
-    __shared__ unsigned long long b_rmax[kMaxCols], b_neval[kMaxCols], b_edges[kMaxCols], b_warn[kMaxCols];
-    __shared__ unsigned int b_claimed, s_k;
-    __shared__ unsigned long long b_urows, b_uent;
-    __shared__ int s_total;
+    __shared__ BlockCounters B;
+    __shared__ WarpTile TT[kLpThreads / 32];
+    __shared__ unsigned long long s_res[4 * kMaxCols];
+    __shared__ double s_fu[kMaxCols];
+    __shared__ long long s_ll[2];
+    __shared__ int s_i[4];
+    __shared__ unsigned int s_u32[4], s_claimed, s_cnt[3], s_base[3];
+    __shared__ unsigned int s_wc[3][kLpThreads / 32];
 
     const int C = P.C;
     const int tid = threadIdx.x;
+    const int lane = tid & 31, warp = tid >> 5;
     const long long gtid = blockIdx.x * (long long)blockDim.x + tid;
     const long long gth = (long long)gridDim.x * blockDim.x;
     LPCtl* ctl = P.ctl;
     unsigned int target = 0;
-    double* sw = smem_dyn;         // [kWin]
-    double* sx = smem_dyn + kWin;  // [kWin * C]
-    const int rows_per_chunk = min(kChunkRows, kLpThreads / C);
+    const int wsm = kWin * (C + 1) + 32;  // doubles of warp-private staging
+    double* sw = smem_dyn + warp * wsm;
+    double* sx = sw + kWin;
+    double* sfu = sx + kWin * C;
+    WarpTile& T = TT[warp];
     const unsigned int allc = C >= 32 ? 0xffffffffu : ((1u << C) - 1u);
-    int* U[2] = {P.U0, P.U1};
-    unsigned int* FM[2] = {P.fmask0, P.fmask1};
+    const unsigned long long pol = l2_evict_last_policy();
+    const int rpw = 32 / C;  // rows per short tile
+    const long long n = P.n;
 
-    // ---- prologue: F0 (engine.py:364-367) is every column's first frontier
+    // ---- prologue: F0 (engine.py:364-367) is every column's first frontier;
+    // the eligible list and F0 are split by row class
     const long long n0 = P.itlp ? 0 : P.ds->n_f0;
     const long long n_el = P.ds->n_elist;
     for (long long i = gtid; i < n0; i += gth) {
         int u = P.f0[i];
-        U[0][i] = u;
-        FM[0][u] = allc;
+        P.fmask[0][u] = allc;
+        // one call site per class: append_u32 aggregates over the converged
+        // threads, which must all target the same list
+        switch (row_class(P.row_len[u])) {
+            case CLS_SHORT: append_u32(P.flist[0][0], &ctl->n_f0[0], u); break;
+            case CLS_LONG: append_u32(P.flist[1][0], &ctl->n_f0[1], u); break;
+            default: append_u32(P.flist[2][0], &ctl->n_f0[2], u); break;
+        }
+    }
+    for (long long i = gtid; i < n_el; i += gth) {
+        int u = P.elist[i];
+        switch (row_class(P.row_len[u])) {
+            case CLS_SHORT: append_u32(P.elist_c[0], &ctl->n_el[0], u); break;
+            case CLS_LONG: append_u32(P.elist_c[1], &ctl->n_el[1], u); break;
+            default: append_u32(P.elist_c[2], &ctl->n_el[2], u); break;
+        }
     }
     if (tid == 0) {
         for (int c = 0; c < C; c++) {
@@ -239,190 +598,201 @@ __global__ void __launch_bounds__(kLpThreads) k_lp_fused(LPParams P) {
             for (int c = 0; c < C; c++) ctl->elig_count[c] = n_el;
     }
     grid_sync(&ctl->bar, target);
-    if (tid == 0) decide_actions(S, P, nullptr, 1);
+    if (tid == 0) decide_actions(S, P, nullptr, nullptr, 1);
+    long long nel[3], ncur[3];
+    for (int j = 0; j < 3; j++) {
+        nel[j] = *(volatile unsigned int*)&ctl->n_el[j];
+        ncur[j] = *(volatile unsigned int*)&ctl->n_f0[j];
+    }
     __syncthreads();
 
-    long long ncur = n0;
     long long R = 0;
     while (!S.done) {
         const unsigned int FR = S.fr_mask, CE = S.cert_mask;
-        RoundSlot* slot = &ctl->slot[R & 1];
-        const int* W = CE ? P.elist : U[R & 1];
-        const long long nwork = CE ? n_el : ncur;
-        unsigned int* fm_cur = FM[R & 1];
-        ClaimCtx K{FM[(R + 1) & 1], U[(R + 1) & 1], &slot->cnt, P.eligm, 0u};
+        const int ri = (int)(R & 1), rn = ri ^ 1;
+        RoundSlot* slot = &ctl->slot[ri];
+        const int* W0 = CE ? P.elist_c[0] : P.flist[0][ri];
+        const int* W1 = CE ? P.elist_c[1] : P.flist[1][ri];
+        const int* W2 = CE ? P.elist_c[2] : P.flist[2][ri];
+        const long long n0c = CE ? nel[0] : ncur[0];
+        const long long n1c = CE ? nel[1] : ncur[1];
+        const long long n2c = CE ? nel[2] : ncur[2];
+        const long long nwork = n0c + n1c + n2c;
+        const bool scan_mode = !P.itlp && nwork * kScanRatio >= n;
+        unsigned int* fm_cur = P.fmask[ri];
+        unsigned int* fm_next = P.fmask[rn];
+        ClaimCtx K{fm_next, {P.flist[0][rn], P.flist[1][rn], P.flist[2][rn]}, slot->cnt, P.eligm, P.row_len, 0u};
         if (tid < kMaxCols) {
-            b_rmax[tid] = 0;
-            b_neval[tid] = 0;
-            b_edges[tid] = 0;
-            b_warn[tid] = 0;
+            B.rmax[tid] = 0;
+            B.neval[tid] = 0;
+            B.edges[tid] = 0;
+            B.warn[tid] = 0;
         }
         if (tid == 0) {
-            b_claimed = 0;
-            b_urows = 0;
-            b_uent = 0;
+            B.claimed = 0;
+            B.urows = 0;
+            B.uent = 0;
         }
         __syncthreads();
 
-        // ======== phase 1: evaluate + expand, chunk by chunk ========
-        for (;;) {
-            if (tid == 0) s_k = atomicAdd(&slot->grab, (unsigned int)rows_per_chunk);
-            __syncthreads();
-            const long long k0 = s_k;
-            if (k0 >= nwork) break;
-            const int nrows = (int)min((long long)rows_per_chunk, nwork - k0);
-            if (tid < kChunkRows) {
-                int len = 0;
-                unsigned int em = 0;
-                int u = -1;
-                long long st = 0;
-                if (tid < nrows) {
-                    u = W[k0 + tid];
-                    em = P.itlp ? (CE & P.eligm[u]) : ((fm_cur[u] & FR) | (CE & P.eligm[u]));
-                    if (em) {
-                        st = P.row_start[u];
-                        len = P.row_len[u];
-                    }
-                    P.emask_store[u] = em;
-                }
-                s_u[tid] = u;
-                s_em[tid] = em;
-                s_st[tid] = st;
-                s_len[tid] = len;
-                s_chg[tid] = 0;
-            }
-            __syncthreads();
-            if (tid < 32) {  // exclusive scan of row lengths (kChunkRows == 32)
-                int x = s_len[tid], incl = x;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    int y = __shfl_up_sync(0xffffffffu, incl, o);
-                    if (tid >= o) incl += y;
-                }
-                s_off[tid] = incl - x;
-                if (tid == 31) s_total = incl;
-            }
-            __syncthreads();
-            const int T = s_total;
-            if (tid == 0) {
-                int nz = 0;
-                for (int r = 0; r < nrows; r++) nz += s_em[r] != 0;
-                b_urows += nz;
-                b_uent += T;
-            }
-            // this thread's (row, column) pair
-            const int pr = tid / C, pc = tid - pr * C;
-            const bool active = pr < nrows && ((s_em[pr] >> pc) & 1u);
-            double fu = 0.0;
-            RowAcc acc;
-            acc.init();
-            if (active) fu = P.X[(long long)s_u[pr] * C + pc];
-            for (int wb = 0; wb < T; wb += kWin) {
-                const int wn = min(kWin, T - wb);
-                for (int t = tid; t < wn; t += kLpThreads) {
-                    int g = wb + t;
-                    int r = row_of(s_off, nrows, g);
-                    long long p = s_st[r] + (g - s_off[r]);
-                    int v = P.nbr[p];
-                    sw[t] = P.w[p];
-                    const double* xv = P.X + (long long)v * C;
-                    double* dst = sx + t * C;
-                    for (int c = 0; c < C; c++) dst[c] = xv[c];
-                }
+        // ======== phase 1: evaluate + expand ========
+        // staging items: short [0, n0c), long [n0c, n0c+n1c), hub [n0c+n1c, nwork)
+        {
+            RoundCtx RH{W2, n0c + n1c, FR, CE, fm_cur, scan_mode};
+            for (;;) {  // hub rows: whole CTA per row (critical path first)
+                if (tid == 0) s_i[2] = (int)atomicAdd(&slot->grab[2], 1u);
                 __syncthreads();
-                if (active) {
-                    int lo = max(s_off[pr], wb) - wb;
-                    int hi = min(s_off[pr] + s_len[pr], wb + wn) - wb;
-                    for (int t = lo; t < hi; t++) {
-                        double x = sx[t * C + pc];
-                        acc.add(sw[t], is_boxed(x) ? boxed_class(x) : -1, x, fu);
-                    }
-                }
+                const int k = s_i[2];
                 __syncthreads();
+                if (k >= n2c) break;
+                cta_hub_row(P, RH, K, B, smem_dyn, s_fu, k, pol, s_i, s_ll, s_u32);
             }
-            if (active) {
-                double val;
-                double d = acc.finish(fu, &val);
-                int u = s_u[pr];
-                P.Y[(long long)u * C + pc] = val;
-                atomicAdd(&b_neval[pc], 1ULL);
-                atomicAdd(&b_edges[pc], (unsigned long long)s_len[pr]);
-                if (d < 0.0) {  // isolated sentinel (_csr.pyx:49-51, 170-173)
-                    atomicAdd(&b_warn[pc], 1ULL);
-                    atomicAnd(&P.eligm[u], ~(1u << pc));
-                    atomicAdd((unsigned long long*)&ctl->elig_count[pc], ~0ULL);
-                } else {
-                    if (d > 0.0) atomicMax(&b_rmax[pc], dbits(d));
-                    if (!P.itlp && d > P.delta) atomicOr(&s_chg[pr], 1u << pc);
-                }
+            RoundCtx RL{W1, n0c, FR, CE, fm_cur, scan_mode};
+            for (;;) {  // long rows: one row per warp tile
+                int k = 0;
+                if (lane == 0) k = (int)atomicAdd(&slot->grab[1], 1u);
+                k = __shfl_sync(0xffffffffu, k, 0);
+                if (k >= n1c) break;
+                warp_tile(P, RL, K, B, T, sw, sx, sfu, k, 1, pol);
+                __syncwarp();
             }
-            __syncthreads();
-            if (!P.itlp) {
-                // expand: changed rows claim themselves and eligible neighbours
-                if (tid < nrows && s_chg[tid]) claim(K, s_u[tid], s_chg[tid]);
-                for (int g = tid; g < T; g += kLpThreads) {
-                    int r = row_of(s_off, nrows, g);
-                    unsigned int chg = s_chg[r];
-                    if (chg) claim(K, P.nbr[s_st[r] + (g - s_off[r])], chg);
-                }
+            RoundCtx RS{W0, 0, FR, CE, fm_cur, scan_mode};
+            for (;;) {  // short rows: rpw rows per warp tile
+                int k = 0;
+                if (lane == 0) k = (int)atomicAdd(&slot->grab[0], (unsigned int)rpw);
+                k = __shfl_sync(0xffffffffu, k, 0);
+                if (k >= n0c) break;
+                warp_tile(P, RS, K, B, T, sw, sx, sfu, k, (int)min((long long)rpw, n0c - k), pol);
+                __syncwarp();
             }
-            __syncthreads();
         }
-        if (K.claimed) atomicOr(&b_claimed, K.claimed);
+        if (K.claimed) atomicOr(&B.claimed, K.claimed);
         __syncthreads();
         if (tid < C) {
-            if (b_rmax[tid]) atomicMax(&slot->rmax[tid], b_rmax[tid]);
-            if (b_neval[tid]) atomicAdd(&slot->neval[tid], b_neval[tid]);
-            if (b_edges[tid]) atomicAdd(&slot->edges[tid], b_edges[tid]);
-            if (b_warn[tid]) atomicAdd(&slot->warn[tid], b_warn[tid]);
+            if (B.rmax[tid]) atomicMax(&slot->rmax[tid], B.rmax[tid]);
+            if (B.neval[tid]) atomicAdd(&slot->neval[tid], B.neval[tid]);
+            if (B.edges[tid]) atomicAdd(&slot->edges[tid], B.edges[tid]);
+            if (B.warn[tid]) atomicAdd(&slot->warn[tid], B.warn[tid]);
         }
         if (tid == 0) {
-            if (b_claimed) atomicOr(&slot->claimed, b_claimed);
-            if (b_urows) atomicAdd(&slot->urows, b_urows);
-            if (b_uent) atomicAdd(&slot->uentries, b_uent);
+            if (B.claimed) atomicOr(&slot->claimed, B.claimed);
+            if (B.urows) atomicAdd(&slot->urows, B.urows);
+            if (B.uent) atomicAdd(&slot->uentries, B.uent);
         }
         grid_sync(&ctl->bar, target);
 
-        // ======== phase 2: commit (Jacobi) and clear this round's masks ========
+        // ======== phase 2: commit (Jacobi), clear this round's masks ========
         for (long long i = gtid; i < nwork; i += gth) {
-            int u = W[i];
+            int u = i < n0c ? W0[i] : (i < n0c + n1c ? W1[i - n0c] : W2[i - n0c - n1c]);
+            if (ctl->seen) {
+                int old = atomicExch(&ctl->seen[u], (int)(R + 1));
+                if (old == (int)(R + 1)) atomicAdd(&ctl->dups, 1ULL);
+            }
             unsigned int em = P.emask_store[u];
             for (int c = 0; c < C; c++)
-                if ((em >> c) & 1u) P.X[(long long)u * C + c] = P.Y[(long long)u * C + c];
+                if ((em >> c) & 1u) st_keep(P.X + (long long)u * C + c, __ldcs(P.Y + i * C + c), pol);
             fm_cur[u] = 0;
         }
+        if (scan_mode) {
+            // compaction of the claimed mask into the next class lists: one
+            // contiguous vertex range per CTA, counted then written, so each CTA
+            // issues a single atomic per list
+            const long long chunk = ((n + gridDim.x - 1) / gridDim.x + 255) & ~255LL;
+            const long long v0 = blockIdx.x * chunk, v1 = min(n, v0 + chunk);
+            unsigned int cc[3] = {0u, 0u, 0u};
+            for (long long v = v0 + tid; v < v1; v += kLpThreads) {
+                unsigned int bits = fm_next[v];
+                if (!bits) continue;
+                if (!(bits & P.eligm[v])) {
+                    fm_next[v] = 0;  // claimed but ineligible: never evaluated
+                    continue;
+                }
+                int cls = row_class(P.row_len[v]);
+                cc[0] += cls == 0;
+                cc[1] += cls == 1;
+                cc[2] += cls == 2;
+            }
+            for (int j = 0; j < 3; j++) {
+                unsigned int x = warp_sum(cc[j]);
+                if (lane == 0) s_wc[j][warp] = x;
+            }
+            __syncthreads();
+            if (tid < 3) {
+                unsigned int tot = 0;
+                for (int w = 0; w < kLpThreads / 32; w++) {
+                    unsigned int x = s_wc[tid][w];
+                    s_wc[tid][w] = tot;
+                    tot += x;
+                }
+                s_base[tid] = tot ? atomicAdd(&slot->cnt[tid], tot) : 0u;
+            }
+            __syncthreads();
+            for (long long vb = v0; vb < v1; vb += kLpThreads) {
+                long long v = vb + tid;
+                unsigned int bits = v < v1 ? fm_next[v] : 0u;
+                int cls = bits ? row_class(P.row_len[v]) : -1;
+                const unsigned int below = (1u << lane) - 1u;
+#pragma unroll
+                for (int j = 0; j < 3; j++) {
+                    unsigned int bj = __ballot_sync(0xffffffffu, cls == j);
+                    if (cls == j) P.flist[j][rn][s_base[j] + s_wc[j][warp] + __popc(bj & below)] = (int)v;
+                    __syncwarp();
+                    if (lane == 0) s_wc[j][warp] += __popc(bj);
+                    __syncwarp();
+                }
+            }
+        }
         if (gtid == 0) {
-            RoundSlot* nx = &ctl->slot[(R + 1) & 1];
+            RoundSlot* nx = &ctl->slot[rn];
             for (int c = 0; c < kMaxCols; c++) nx->rmax[c] = nx->neval[c] = nx->edges[c] = nx->warn[c] = 0;
             nx->claimed = 0;
             nx->urows = 0;
             nx->uentries = 0;
-            nx->grab = 0;
-            nx->cnt = 0;
+            for (int j = 0; j < 3; j++) nx->grab[j] = nx->cnt[j] = 0;
         }
         grid_sync(&ctl->bar, target);
-        if (tid == 0) {
-            RoundSlot res;
+        // controller: stage the slot's per-column results in shared memory
+        // (parallel loads), then one thread replays the state machines
+        {
             const volatile RoundSlot* vs = slot;
-            for (int c = 0; c < C; c++) {
-                res.rmax[c] = vs->rmax[c];
-                res.neval[c] = vs->neval[c];
-                res.edges[c] = vs->edges[c];
-                res.warn[c] = vs->warn[c];
+            if (tid < C) {
+                s_res[tid] = vs->rmax[tid];
+                s_res[kMaxCols + tid] = vs->neval[tid];
+                s_res[2 * kMaxCols + tid] = vs->edges[tid];
+                s_res[3 * kMaxCols + tid] = vs->warn[tid];
             }
-            res.claimed = vs->claimed;
-            decide_actions(S, P, &res, 0);
-            if (blockIdx.x == 0) {
+            if (tid == 32) s_claimed = vs->claimed;
+            if (tid >= 64 && tid < 67) s_cnt[tid - 64] = vs->cnt[tid - 64];
+            if (blockIdx.x == 0 && tid == 128) {
                 ctl->urows += (long long)vs->urows;
                 ctl->uentries += (long long)vs->uentries;
             }
+            __syncthreads();
+            if (tid == 0) decide_actions(S, P, s_res, &s_claimed, 0);
         }
-        ncur = *(volatile unsigned int*)&slot->cnt;
+        for (int j = 0; j < 3; j++) ncur[j] = s_cnt[j];
+        if (ctl->trace && gtid == 0 && R < ctl->trace_cap) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            unsigned long long* e = ctl->trace + 4 * R;
+            e[0] = (unsigned long long)n0c;
+            e[1] = (unsigned long long)(n1c + (n2c << 32));
+            e[2] = (unsigned long long)FR | ((unsigned long long)CE << 16) | ((unsigned long long)scan_mode << 32);
+            e[3] = t;
+        }
         R++;
         __syncthreads();
     }
     // leftover frontiers (budget exhausted): clear their masks for the next batch
-    for (long long i = gtid; i < ncur; i += gth) FM[R & 1][U[R & 1][i]] = 0;
+    {
+        const int ri = (int)(R & 1);
+        for (long long i = gtid; i < ncur[0] + ncur[1] + ncur[2]; i += gth) {
+            int u = i < ncur[0] ? P.flist[0][ri][i]
+                                : (i < ncur[0] + ncur[1] ? P.flist[1][ri][i - ncur[0]]
+                                                         : P.flist[2][ri][i - ncur[0] - ncur[1]]);
+            P.fmask[ri][u] = 0;
+        }
+    }
     if (gtid == 0) {
         for (int c = 0; c < C; c++) {
             ctl->iterations[c] = S.iterations[c];
@@ -440,7 +810,7 @@ __global__ void __launch_bounds__(kLpThreads) k_lp_fused(LPParams P) {
 void lp_setup(Engine& E) {
     if (E.lp_grid) return;
     if (E.ncol > kMaxCols) throw CudaFailure(cudaErrorInvalidValue, "ncol > kMaxCols", __FILE__, __LINE__);
-    E.lp_smem = (size_t)kWin * (E.ncol + 1) * sizeof(double);
+    E.lp_smem = (size_t)(kLpThreads / 32) * (kWin * (E.ncol + 1) + 32) * sizeof(double);
     DLP_CUDA_TRY(cudaFuncSetAttribute(k_lp_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)E.lp_smem));
     int occ = 0;
     DLP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_lp_fused, kLpThreads, E.lp_smem));
@@ -448,6 +818,15 @@ void lp_setup(Engine& E) {
     if (occ > 8) occ = 8;
     E.lp_grid = E.sm_count * occ;
     if (const char* g = getenv("DLP_LP_GRID")) E.lp_grid = atoi(g);
+    E.lp_trace_path = getenv("DLP_LP_TRACE");
+    if (const char* v = getenv("DLP_LONG_ROW")) {
+        int x = atoi(v);
+        DLP_CUDA_TRY(cudaMemcpyToSymbol(c_long_row, &x, sizeof(int)));
+    }
+    if (const char* v = getenv("DLP_HUB_ROW")) {
+        int x = atoi(v);
+        DLP_CUDA_TRY(cudaMemcpyToSymbol(c_hub_row, &x, sizeof(int)));
+    }
     for (auto& ev : E.lp_ev) DLP_CUDA_TRY(cudaEventCreate(&ev));
 }
 
@@ -462,25 +841,57 @@ void lp_run_dev(Engine& E, double delta, long long max_iter, bool itlp) {
     P.Y = E.f[1].p;
     P.eligm = E.eligm.p;
     P.emask_store = E.emask_store.p;
-    P.fmask0 = E.fmask[0].p;
-    P.fmask1 = E.fmask[1].p;
-    P.U0 = E.ulist[0].p;
-    P.U1 = E.ulist[1].p;
+    for (int i = 0; i < 2; i++) {
+        P.fmask[i] = E.fmask[i].p;
+        P.flist[0][i] = E.ulist[i].p;
+        P.flist[1][i] = E.llist[i].p;
+        P.flist[2][i] = E.hlist[i].p;
+    }
+    P.elist_c[0] = E.elist_s.p;
+    P.elist_c[1] = E.elist_l.p;
+    P.elist_c[2] = E.elist_h.p;
     P.f0 = E.f0.p;
     P.elist = E.elist.p;
     P.ds = E.ds;
     P.ctl = E.ctl;
     P.delta = delta;
     P.max_iter = max_iter;
+    P.n = E.n_slots;
     P.C = E.ncol;
     P.itlp = itlp ? 1 : 0;
     DLP_CUDA_TRY(cudaMemsetAsync(E.ctl, 0, sizeof(LPCtl), E.st));
+    if (E.lp_trace_path) {
+        const long long cap = 1 << 16;
+        E.lp_trace.reserve(4 * cap + 4, 0, E.st);
+        unsigned long long* tp = E.lp_trace.p;
+        DLP_CUDA_TRY(cudaMemcpyAsync(&E.ctl->trace, &tp, sizeof(tp), cudaMemcpyHostToDevice, E.st));
+        DLP_CUDA_TRY(cudaMemcpyAsync(&E.ctl->trace_cap, &cap, sizeof(cap), cudaMemcpyHostToDevice, E.st));
+        E.lp_seen.reserve(E.cap_n + 1, 0, E.st);
+        DLP_CUDA_TRY(cudaMemsetAsync(E.lp_seen.p, 0, (E.cap_n + 1) * sizeof(int), E.st));
+        int* sp = E.lp_seen.p;
+        DLP_CUDA_TRY(cudaMemcpyAsync(&E.ctl->seen, &sp, sizeof(sp), cudaMemcpyHostToDevice, E.st));
+        DLP_CUDA_TRY(cudaStreamSynchronize(E.st));  // host values above are stack temporaries
+    }
     void* args[] = {&P};
     DLP_CUDA_TRY(cudaEventRecord(E.lp_ev[0], E.st));
     DLP_CUDA_TRY(cudaLaunchCooperativeKernel((void*)k_lp_fused, dim3(E.lp_grid), dim3(kLpThreads), args, E.lp_smem,
                                              E.st));
     DLP_CUDA_TRY(cudaEventRecord(E.lp_ev[1], E.st));
     E.launches++;
+}
+
+// Append the last launch's per-round trace to $DLP_LP_TRACE (diagnostics).
+void lp_dump_trace(Engine& E, long long rounds) {
+    if (!E.lp_trace_path || rounds <= 0) return;
+    long long n = std::min<long long>(rounds, 1 << 16);
+    std::vector<unsigned long long> h(4 * n);
+    DLP_CUDA_TRY(cudaMemcpy(h.data(), E.lp_trace.p, h.size() * 8, cudaMemcpyDeviceToHost));
+    FILE* fp = fopen(E.lp_trace_path, "a");
+    if (!fp) return;
+    fprintf(fp, "# launch rounds=%lld grid=%d dups=%llu\n", rounds, E.lp_grid, E.h_ctl.p->dups);
+    for (long long r = 0; r < n; r++)
+        fprintf(fp, "%lld %llu %llu %llx %llu\n", r, h[4 * r], h[4 * r + 1], h[4 * r + 2], h[4 * r + 3]);
+    fclose(fp);
 }
 
 // ---------------------------------------------------------------------------

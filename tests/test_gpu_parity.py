@@ -198,3 +198,19 @@ def test_bitwise_repeatable(gpu_device):
         blobs.add(lab.f.tobytes())
         g.close()
     assert len(blobs) == 1
+
+
+@pytest.mark.parametrize("ncls,long_row,hub_row", [(10, 8, 24), (2, 12, 30), (10, 0, 0)])
+def test_row_class_paths(gpu_device, ncls, long_row, hub_row):
+    """The LP kernel's short (multi-row warp tiles), long (single-row warp
+    tiles) and hub (CTA-cooperative, double-buffered) paths, forced to mix in
+    the same rounds by low thresholds, stay bit-identical to the oracle."""
+    import os
+    import subprocess
+    import sys
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    env = dict(os.environ, DLP_LONG_ROW=str(long_row), DLP_HUB_ROW=str(hub_row))
+    r = subprocess.run([sys.executable, os.path.join(here, "_row_class_check.py"), str(ncls)], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
