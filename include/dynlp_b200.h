@@ -108,6 +108,11 @@ int dlp_apply_structure(dlp_engine* e, const dlp_batch* batch);
 int dlp_itlp_batch(dlp_engine* e, const dlp_config* cfg, const dlp_batch* batch,
                    dlp_report* reports);
 
+/* Capacity hint (like std::vector::reserve): size vertex arrays, the edge
+ * log and the adjacency pool for n_vertices slots and n_edges live edges so
+ * later batches never reallocate.  Optional; growth is otherwise geometric. */
+int dlp_reserve(dlp_engine* e, int64_t n_vertices, int64_t n_edges);
+
 /* DynamicGraph.num_slots / num_alive (graph.py:189-192, 182). */
 int dlp_num_slots(dlp_engine* e, int64_t* n_slots, int64_t* num_alive);
 /* LabelState.f / .gt (labels.py:21-22).  f is [columns][n] row-major; GT

@@ -56,6 +56,7 @@ SIGNATURES = {
     "dlp_apply_batch_device": (_int, [_p, _p, _p, _int, _p]),
     "dlp_apply_structure": (_int, [_p, _p]),
     "dlp_itlp_batch": (_int, [_p, _p, _p, _p]),
+    "dlp_reserve": (_int, [_p, _i64, _i64]),
     "dlp_num_slots": (_int, [_p, _p, _p]),
     "dlp_read_labels": (_int, [_p, _p, _p, _i64]),
     "dlp_write_labels": (_int, [_p, _p, _i64]),

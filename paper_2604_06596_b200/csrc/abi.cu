@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -24,6 +25,15 @@ struct dlp_engine {
     Engine E;
     bool poisoned = false;
 };
+
+namespace dlp {
+void host_mark(Engine& E, const char* what) {
+    if (!E.host_trace) return;
+    double t = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+    fprintf(stderr, "[dlp host] %-14s +%.3f ms\n", what, t - E.host_t0);
+    E.host_t0 = t;
+}
+}  // namespace dlp
 
 namespace {
 
@@ -238,6 +248,10 @@ int run_batch(dlp_engine* h, const dlp_config* cfg, const dlp_batch* batch, bool
             int rc = validate_batch(E, hb);
             if (rc) return rc;
         }
+        if (E.host_trace) {
+            E.host_t0 = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+            host_mark(E, "validated");
+        }
         long long base = E.n_slots, k = hb.k, ne = hb.ne, nd = hb.nd;
         ensure_vertex_capacity(E, base + k + 1);
         ensure_log(E, E.live_edges + ne + 1);
@@ -256,6 +270,7 @@ int run_batch(dlp_engine* h, const dlp_config* cfg, const dlp_batch* batch, bool
         } else {
             bd = stage_batch(E, hb);
         }
+        host_mark(E, "staged");
         long long launches0 = E.launches;
         k_reset_batch<<<1, 1, 0, E.st>>>(E.ds);
         E.launches++;
@@ -302,6 +317,7 @@ int run_batch(dlp_engine* h, const dlp_config* cfg, const dlp_batch* batch, bool
             E.cc_valid = false;
         }
         DLP_CUDA_TRY(cudaGetLastError());
+        host_mark(E, "enqueued");
         DLP_CUDA_TRY(cudaMemcpyAsync(E.h_ds.p, E.ds, sizeof(DevState), cudaMemcpyDeviceToHost, E.st));
         DLP_CUDA_TRY(cudaMemcpyAsync(E.h_ctl.p, E.ctl, sizeof(LPCtl), cudaMemcpyDeviceToHost, E.st));
         DLP_CUDA_TRY(cudaStreamSynchronize(E.st));
@@ -313,6 +329,7 @@ int run_batch(dlp_engine* h, const dlp_config* cfg, const dlp_batch* batch, bool
         if (E.pool_top_host > E.pool_cap) return fail(E, DLP_EINTERNAL, "adjacency pool overflow");
         float lp_ms = 0.f;
         DLP_CUDA_TRY(cudaEventElapsedTime(&lp_ms, E.lp_ev[0], E.lp_ev[1]));
+        host_mark(E, "synced");
         const LPCtl& L = *E.h_ctl.p;
         lp_dump_trace(E, L.rounds);
         for (int c = 0; c < E.ncol; c++) {
@@ -363,9 +380,16 @@ int dlp_create(const dlp_config* cfg, int device, dlp_engine** out) {
             delete h;
             return DLP_ECUDA;
         }
+        E.host_trace = getenv("DLP_HOST_TRACE") != nullptr;
         E.num_classes = cfg && cfg->num_classes > 2 ? cfg->num_classes : 2;
         E.ncol = E.num_classes > 2 ? E.num_classes : 1;
         DLP_CUDA_TRY(cudaStreamCreateWithFlags(&E.st, cudaStreamNonBlocking));
+        {  // keep freed stream-ordered allocations cached in the device pool
+            cudaMemPool_t mp;
+            DLP_CUDA_TRY(cudaDeviceGetDefaultMemPool(&mp, device));
+            unsigned long long thr = ~0ULL;
+            DLP_CUDA_TRY(cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &thr));
+        }
         DLP_CUDA_TRY(cudaMalloc(&E.ds, sizeof(DevState)));
         DLP_CUDA_TRY(cudaMemset(E.ds, 0, sizeof(DevState)));
         if (E.ncol > kMaxCols) {
@@ -390,6 +414,24 @@ int dlp_create(const dlp_config* cfg, int device, dlp_engine** out) {
     return DLP_OK;
 }
 
+int dlp_reserve(dlp_engine* h, int64_t n_vertices, int64_t n_edges) {
+    if (!h) return DLP_EINTERNAL;
+    Engine& E = h->E;
+    if (h->poisoned) return fail(E, DLP_EINTERNAL, "engine is unusable after an earlier CUDA error");
+    if (n_vertices < 0 || n_edges < 0) return fail(E, DLP_EVALIDATION, "reserve sizes must be nonnegative");
+    try {
+        DLP_CUDA_TRY(cudaSetDevice(E.device));
+        ensure_vertex_capacity(E, n_vertices + 1);
+        ensure_log(E, n_edges + 1);
+        long long want = 2 * n_edges + (2 * n_edges) / 2 + 4 * n_vertices;
+        if (E.pool_cap < want) compact_pool(E, want - 2 * E.live_edges);
+        DLP_CUDA_TRY(cudaStreamSynchronize(E.st));
+    } catch (const CudaFailure& f) {
+        return cuda_fail(h, f);
+    }
+    return DLP_OK;
+}
+
 int dlp_destroy(dlp_engine* h) {
     if (!h) return DLP_OK;
     Engine& E = h->E;
@@ -402,11 +444,11 @@ int dlp_destroy(dlp_engine* h) {
     E.row_start.release();
     DevArray<int>* i32s[] = {&E.row_len, &E.row_up, &E.row_cap, &E.parent, &E.cnt_up, &E.cnt_dn, &E.grp_start,
                              &E.ulist[0], &E.ulist[1], &E.llist[0], &E.llist[1], &E.hlist[0], &E.hlist[1], &E.elist_s, &E.elist_l, &E.elist_h, &E.f0, &E.elist, &E.purge_list, &E.touched,
-                             &E.nbr, &E.log_lo, &E.log_hi, &E.log_lo2, &E.log_hi2, &E.val_a, &E.val_b,
+                             &E.nbr, &E.nbr_sp, &E.log_lo, &E.log_hi, &E.log_lo2, &E.log_hi2, &E.val_a, &E.val_b,
                              &E.flag_i, &E.pos_i, &E.m_lo, &E.m_hi, &E.mlo_at, &E.mhi_at, &E.lpar, &E.comp,
                              &E.comp_sorted_i, &E.root_flag, &E.root_rank, &E.root_tmp};
     for (auto* a : i32s) a->release();
-    DevArray<double>* f64s[] = {&E.f[0], &E.f[1], &E.wgt, &E.log_w, &E.log_w2, &E.m_w, &E.ew_lo, &E.ew_hi,
+    DevArray<double>* f64s[] = {&E.f[0], &E.f[1], &E.wgt, &E.wgt_sp, &E.log_w, &E.log_w2, &E.m_w, &E.ew_lo, &E.ew_hi,
                                 &E.mw_at, &E.per0, &E.per1, &E.cinit, &E.tau_scratch};
     for (auto* a : f64s) a->release();
     DevArray<unsigned int>* u32s[] = {&E.eligm, &E.emask_store, &E.fmask[0], &E.fmask[1]};

@@ -60,6 +60,18 @@ struct RowAcc {
         else
             s = __dadd_rn(s, __dmul_rn(__dsub_rn(fv, fu), w));
     }
+    // same, with x = the NaN-boxed label word of the neighbour
+    __device__ inline void add_boxed(double w, double x, double fu) {
+        w_all = __dadd_rn(w_all, w);
+        if (is_boxed(x)) {
+            if (boxed_class(x) == 0)
+                w0 = __dadd_rn(w0, w);
+            else
+                w1 = __dadd_rn(w1, w);
+        } else {
+            s = __dadd_rn(s, __dmul_rn(__dsub_rn(x, fu), w));
+        }
+    }
     // returns |fn - fu| or -1 for the isolated sentinel (value 0.5)
     __device__ inline double finish(double fu, double* out_val) const {
         if (w_all <= 0.0) {

@@ -44,6 +44,7 @@ struct DevState {
     long long intra_nc;           // intra-batch component count
     double tau;
     long long log_n_before;
+    unsigned long long pool_need;  // relocation space the batch's touched rows need
 };
 
 constexpr int kMaxCols = 16;  // label columns handled by the fused LP kernel
@@ -96,18 +97,17 @@ struct DevArray {
         p = nullptr;
         n = 0;
     }
-    // grow to at least `want` elements, preserving the first `keep` elements
+    // grow to at least `want` elements, preserving the first `keep` elements.
+    // Stream-ordered (cudaMallocAsync / cudaFreeAsync on the engine stream,
+    // memory pool with an unbounded release threshold): no device-wide sync.
     void reserve(size_t want, size_t keep, cudaStream_t st) {
         if (want <= n) return;
         size_t nn = n ? n : 1024;
         while (nn < want) nn += nn / 2 + 1024;
         T* q = nullptr;
-        DLP_CUDA_TRY(cudaMalloc(&q, nn * sizeof(T)));
+        DLP_CUDA_TRY(cudaMallocAsync((void**)&q, nn * sizeof(T), st));
         if (p && keep) DLP_CUDA_TRY(cudaMemcpyAsync(q, p, keep * sizeof(T), cudaMemcpyDeviceToDevice, st));
-        if (p) {
-            DLP_CUDA_TRY(cudaStreamSynchronize(st));
-            cudaFree(p);
-        }
+        if (p) DLP_CUDA_TRY(cudaFreeAsync(p, st));
         p = q;
         n = nn;
     }
@@ -168,8 +168,8 @@ struct Engine {
     DevArray<unsigned int> eligm, emask_store, fmask[2];
     DevArray<int> ulist[2], llist[2], hlist[2], elist_s, elist_l, elist_h, f0, elist, purge_list, touched;
     // adjacency pool ------------------------------------------------------
-    DevArray<int> nbr;
-    DevArray<double> wgt;
+    DevArray<int> nbr, nbr_sp;      // adjacency pool and its compaction target
+    DevArray<double> wgt, wgt_sp;
     long long pool_cap = 0, pool_top_host = 0;
     // edge log ------------------------------------------------------------
     DevArray<int> log_lo, log_hi, log_lo2, log_hi2;
@@ -200,6 +200,8 @@ struct Engine {
     // instrumentation: kernel launches issued and LP kernel time per column
     long long launches = 0;
     cudaEvent_t lp_ev[2] = {nullptr, nullptr};
+    bool host_trace = false;  // DLP_HOST_TRACE: per-phase host timings on stderr
+    double host_t0 = 0.0;
 };
 
 // graph.cu ------------------------------------------------------------------
@@ -213,6 +215,7 @@ void intra_components_dev(Engine& E, const BatchDev& b, long long base);
 void init_components_dev(Engine& E, const BatchDev& b, long long base);
 void reach_and_pin_dev(Engine& E, bool full_rebuild, long long n);
 void compact_pool(Engine& E, long long min_free);
+void host_mark(Engine& E, const char* what);
 // lp.cu ---------------------------------------------------------------------
 void lp_run_dev(Engine& E, double delta, long long max_iter, bool itlp);
 void lp_setup(Engine& E);

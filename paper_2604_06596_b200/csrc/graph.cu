@@ -392,6 +392,20 @@ __global__ void k_group_heads(const unsigned long long* skey, long long n2, cons
     }
 }
 
+// relocation space needed by the touched rows (same rule as k_row_alloc)
+__global__ void k_pool_need(const int* touched, DevState* ds, const int* row_len, const int* row_cap,
+                            const int* cnt_up, const int* cnt_dn) {
+    long long nt = ds->n_touched;
+    unsigned long long sum = 0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nt; i += (long long)gridDim.x * blockDim.x) {
+        int x = touched[i];
+        int need = row_len[x] + cnt_up[x] + cnt_dn[x];
+        if (need > row_cap[x]) sum += (unsigned long long)(need + need / 2 + 4);
+    }
+    sum = warp_sum(sum);
+    if ((threadIdx.x & 31) == 0 && sum) atomicAdd(&ds->pool_need, sum);
+}
+
 // thread per touched row: make room for the new up entries (and, for a new
 // vertex, its down entries); relocate the row when its capacity is exceeded.
 __global__ void k_row_alloc(const int* touched, DevState* ds, long long* row_start, int* row_len, int* row_up,
@@ -507,6 +521,22 @@ void apply_inserts_dev(Engine& E, const BatchDev& b, long long base) {
     cub_sort_pairs(E, E.key_a.p, E.key_b.p, E.val_a.p, E.val_b.p, 2 * ne, std::min(64, bits_for(2 * N + 2)));
     k_group_heads<<<grid_for(2 * ne), kBlock, 0, st>>>(E.key_b.p, 2 * ne, E.ds, E.grp_start.p, E.touched.p, E.ds);
     E.launches++;
+    // exact allocation check (one small read-back): compact / grow the pool
+    // only when this batch's relocations would not fit
+    DLP_CUDA_TRY(cudaMemsetAsync(&E.ds->pool_need, 0, sizeof(unsigned long long), st));
+    k_pool_need<<<grid_for(b.k + ne), kBlock, 0, st>>>(E.touched.p, E.ds, E.row_len.p, E.row_cap.p, E.cnt_up.p,
+                                                       E.cnt_dn.p);
+    E.launches++;
+    DLP_CUDA_TRY(cudaMemcpyAsync(E.h_ds.p, E.ds, sizeof(DevState), cudaMemcpyDeviceToHost, st));
+    DLP_CUDA_TRY(cudaStreamSynchronize(st));
+    {
+        long long need = (long long)E.h_ds.p->pool_need, top = (long long)E.h_ds.p->pool_top;
+        if (top + need > E.pool_cap) {
+            host_mark(E, "pre-compact");
+            compact_pool(E, std::max<long long>(16 * need, E.pool_cap / 4));
+            host_mark(E, "compact");
+        }
+    }
     k_row_alloc<<<grid_for(b.k + ne), kBlock, 0, st>>>(E.touched.p, E.ds, E.row_start.p, E.row_len.p, E.row_up.p,
                                                        E.row_cap.p, E.cnt_up.p, E.cnt_dn.p, E.nbr.p, E.wgt.p);
     E.launches++;
@@ -541,6 +571,7 @@ __global__ void k_repack(const long long* row_start, const int* row_len, const u
             nbr2[d + e] = nbr[s + e];
             w2[d + e] = w[s + e];
         }
+        __syncwarp();  // every lane has read row_start[v] (updated in place)
         if (lane == 0) {
             row_start2[v] = d;
             row_cap2[v] = newcap[v];
@@ -548,16 +579,19 @@ __global__ void k_repack(const long long* row_start, const int* row_len, const u
     }
 }
 
+// Order-preserving repack of every live row into the spare pool (rows packed
+// in vertex order with 25% slack), then swap pools.  The spare has the same
+// capacity as the pool, so a compaction allocates nothing unless the live
+// adjacency itself outgrew the pool (then both grow geometrically).
 void compact_pool(Engine& E, long long min_free) {
     cudaStream_t st = E.st;
     long long n = E.n_slots;
     long long live = 2 * E.live_edges;
     long long need = live + live / 4 + 4 * n + min_free + (1 << 20);
-    if (need < E.pool_cap) need = E.pool_cap;  // never shrink below the current size
-    int* nbr2 = nullptr;
-    double* w2 = nullptr;
-    DLP_CUDA_TRY(cudaMalloc(&nbr2, need * sizeof(int)));
-    DLP_CUDA_TRY(cudaMalloc(&w2, need * sizeof(double)));
+    long long cap = E.pool_cap;
+    if (need > cap) cap = std::max<long long>(need, cap + cap / 2);
+    E.nbr_sp.reserve(cap, 0, st);
+    E.wgt_sp.reserve(cap, 0, st);
     long long top = 0;
     if (n > 0) {
         E.flag_i.reserve(n + 1, 0, st);
@@ -565,44 +599,34 @@ void compact_pool(Engine& E, long long min_free) {
         k_new_caps<<<grid_for(n), kBlock, 0, st>>>(E.row_len.p, E.alive.p, n, E.flag_i.p);
         E.launches++;
         cub_scan(E, E.flag_i.p, E.pos_i.p, n);
-        long long* rs2 = nullptr;
-        int* rc2 = nullptr;
-        DLP_CUDA_TRY(cudaMalloc(&rs2, E.row_start.n * sizeof(long long)));
-        DLP_CUDA_TRY(cudaMalloc(&rc2, E.row_cap.n * sizeof(int)));
-        DLP_CUDA_TRY(cudaMemsetAsync(rs2, 0, E.row_start.n * sizeof(long long), st));
-        DLP_CUDA_TRY(cudaMemsetAsync(rc2, 0, E.row_cap.n * sizeof(int), st));
         k_repack<<<grid_for(n * 32), kBlock, 0, st>>>(E.row_start.p, E.row_len.p, E.alive.p, n, E.flag_i.p, E.pos_i.p,
-                                                      E.nbr.p, E.wgt.p, nbr2, w2, rs2, rc2);
+                                                      E.nbr.p, E.wgt.p, E.nbr_sp.p, E.wgt_sp.p, E.row_start.p,
+                                                      E.row_cap.p);
         E.launches++;
         int last_pos = 0, last_cap = 0;
         DLP_CUDA_TRY(cudaMemcpyAsync(&last_pos, E.pos_i.p + n - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
         DLP_CUDA_TRY(cudaMemcpyAsync(&last_cap, E.flag_i.p + n - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
         DLP_CUDA_TRY(cudaStreamSynchronize(st));
         top = (long long)last_pos + last_cap;
-        cudaFree(E.row_start.p);
-        cudaFree(E.row_cap.p);
-        E.row_start.p = rs2;
-        E.row_cap.p = rc2;
     }
-    DLP_CUDA_TRY(cudaStreamSynchronize(st));
-    if (E.nbr.p) cudaFree(E.nbr.p);
-    if (E.wgt.p) cudaFree(E.wgt.p);
-    E.nbr.p = nbr2;
-    E.nbr.n = need;
-    E.wgt.p = w2;
-    E.wgt.n = need;
-    E.pool_cap = need;
+    std::swap(E.nbr, E.nbr_sp);
+    std::swap(E.wgt, E.wgt_sp);
+    // the new spare must match the pool's capacity for the next compaction
+    E.nbr_sp.reserve(E.nbr.n, 0, st);
+    E.wgt_sp.reserve(E.wgt.n, 0, st);
+    E.pool_cap = (long long)std::min(E.nbr.n, E.wgt.n);
     E.pool_top_host = top;
     unsigned long long t = (unsigned long long)top;
     DLP_CUDA_TRY(cudaMemcpyAsync(&E.ds->pool_top, &t, sizeof(t), cudaMemcpyHostToDevice, st));
     DLP_CUDA_TRY(cudaStreamSynchronize(st));
 }
 
-// Worst case a batch allocates: every touched row relocates with 1.5x slack.
+// The exact per-batch check runs inside apply_inserts_dev (k_pool_need); the
+// host only makes sure the pool exists.
 void ensure_pool(Engine& E, long long new_edges, long long new_vertices) {
-    long long bound = 3 * (2 * E.live_edges + 2 * new_edges) / 2 + 4 * (new_vertices + 2 * new_edges) + 1024;
-    if (E.pool_cap - E.pool_top_host >= bound) return;
-    compact_pool(E, 2 * bound);
+    (void)new_edges;
+    (void)new_vertices;
+    if (E.pool_cap == 0) compact_pool(E, 1 << 16);
 }
 
 // ---------------------------------------------------------------------------

@@ -122,6 +122,30 @@ __device__ inline void st_keep(double* p, double v, unsigned long long pol) {
 }
 
 // warp-aggregated append: every converged caller must pass the same list/count
+// cp.async (LDGSTS) global -> shared with the label L2 policy
+__device__ inline void cp_async8(double* dst, const double* src, unsigned long long pol) {
+    unsigned int d = (unsigned int)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "l"(pol)
+                 : "memory");
+}
+__device__ inline void cp_async16(double* dst, const double* src, unsigned long long pol) {
+    unsigned int d = (unsigned int)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "l"(pol)
+                 : "memory");
+}
+__device__ inline void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// copy the C-wide label vector of one vertex (16-byte chunks when C is even:
+// rows start 16-byte aligned in both global and shared memory)
+__device__ inline void copy_label_row(double* dst, const double* src, int C, unsigned long long pol) {
+    if ((C & 1) == 0) {
+        for (int q = 0; q < C; q += 2) cp_async16(dst + q, src + q, pol);
+    } else {
+        for (int q = 0; q < C; q++) cp_async8(dst + q, src + q, pol);
+    }
+}
+
+// warp-aggregated append: every converged caller must pass the same list/count
 __device__ inline void append_u32(int* list, unsigned int* count, int v) {
     cg::coalesced_group g = cg::coalesced_threads();
     unsigned int base = 0;
@@ -336,36 +360,21 @@ __device__ void warp_tile(const LPParams& P, const RoundCtx& R, ClaimCtx& K, Blo
                 ww[j] = __ldcs(P.w + p);
             }
         }
+        // label rows: asynchronous copies straight into shared memory, so every
+        // gather of the window is in flight at once (no register dependency)
 #pragma unroll
         for (int j = 0; j < kWin / 32; j++) {
             if (rr[j] < 0) continue;
-            int i = lane + 32 * j, r = rr[j];
-            unsigned int emr = T.em[r];
+            int i = lane + 32 * j;
             sw[i] = ww[j];
-            const double* xv = P.X + (long long)vv[j] * C;
-            for (int c = 0; c < C; c++) {
-                if (!((emr >> c) & 1u)) continue;
-                double x = ld_keep(xv + c, pol);
-                // product terms are independent: precompute them here, the ordered
-                // sums below keep the reference's summation order
-                sx[i * C + c] = is_boxed(x) ? x : __dmul_rn(__dsub_rn(x, sfu[r * C + c]), ww[j]);
-            }
+            copy_label_row(sx + i * C, P.X + (long long)vv[j] * C, C, pol);
         }
+        cp_async_wait_all();
         __syncwarp();
         if (aact) {
+            const double fu = sfu[ar * C + ac];
             const int lo = max(a_lo, wb) - wb, hi = min(a_hi, wb + wn) - wb;
-            for (int t = lo; t < hi; t++) {
-                double w = sw[t], x = sx[t * C + ac];
-                acc.w_all = __dadd_rn(acc.w_all, w);
-                if (is_boxed(x)) {
-                    if (boxed_class(x) == 0)
-                        acc.w0 = __dadd_rn(acc.w0, w);
-                    else
-                        acc.w1 = __dadd_rn(acc.w1, w);
-                } else {
-                    acc.s = __dadd_rn(acc.s, x);
-                }
-            }
+            for (int t = lo; t < hi; t++) acc.add_boxed(sw[t], sx[t * C + ac], fu);
         }
         __syncwarp();
     }
@@ -456,15 +465,10 @@ __device__ void cta_hub_row(const LPParams& P, const RoundCtx& R, ClaimCtx& K, B
         for (int i = t0; i < wn; i += nth) {
             long long p = st + wb + i;
             int v = __ldcs(P.nbr + p);
-            double wt = __ldcs(P.w + p);
-            sw[i] = wt;
-            const double* xv = P.X + (long long)v * C;
-            for (int c = 0; c < C; c++) {
-                if (!((em >> c) & 1u)) continue;
-                double x = ld_keep(xv + c, pol);
-                sx[i * C + c] = is_boxed(x) ? x : __dmul_rn(__dsub_rn(x, s_fu[c]), wt);
-            }
+            sw[i] = __ldcs(P.w + p);
+            copy_label_row(sx + i * C, P.X + (long long)v * C, C, pol);
         }
+        cp_async_wait_all();
     };
     gather(0, tid, kLpThreads);
     __syncthreads();
@@ -478,18 +482,8 @@ __device__ void cta_hub_row(const LPParams& P, const RoundCtx& R, ClaimCtx& K, B
             const double* sw = buf + (w & 1) * bsz;
             const double* sx = sw + kHubWin;
             const int wn = min(kHubWin, len - w * kHubWin);
-            for (int t = 0; t < wn; t++) {
-                double wt = sw[t], x = sx[t * C + tid];
-                acc.w_all = __dadd_rn(acc.w_all, wt);
-                if (is_boxed(x)) {
-                    if (boxed_class(x) == 0)
-                        acc.w0 = __dadd_rn(acc.w0, wt);
-                    else
-                        acc.w1 = __dadd_rn(acc.w1, wt);
-                } else {
-                    acc.s = __dadd_rn(acc.s, x);
-                }
-            }
+            const double fu = s_fu[tid];
+            for (int t = 0; t < wn; t++) acc.add_boxed(sw[t], sx[t * C + tid], fu);
         }
         __syncthreads();
     }

@@ -150,6 +150,11 @@ class DynamicGraph:
         except Exception:
             pass
 
+    def reserve(self, n_vertices: int, n_edges: int) -> None:
+        """Capacity hint: pre-size device arrays for n_vertices slots and
+        n_edges live edges (no reallocation inside later batches)."""
+        self._check(self._lib.dlp_reserve(self._h, int(n_vertices), int(n_edges)))
+
     # -- accessors mirroring graph.py ------------------------------------------------
     def _counts(self):
         n, a = C.c_int64(), C.c_int64()
