@@ -565,7 +565,7 @@ int dlp_read_eligible(dlp_engine* h, uint8_t* elig, int64_t n) {
     try {
         std::vector<unsigned int> m(n);
         if (n) DLP_CUDA_TRY(cudaMemcpy(m.data(), E.eligm.p, n * sizeof(unsigned int), cudaMemcpyDeviceToHost));
-        for (long long v = 0; v < n; v++) elig[v] = m[v] != 0;
+        for (long long v = 0; v < n; v++) elig[v] = (m[v] & 0xFFFFu) != 0;  // column bits (LP keeps the row class above)
     } catch (const CudaFailure& e) {
         return cuda_fail(h, e);
     }

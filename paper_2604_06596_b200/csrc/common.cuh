@@ -60,17 +60,18 @@ struct RowAcc {
         else
             s = __dadd_rn(s, __dmul_rn(__dsub_rn(fv, fu), w));
     }
-    // same, with x = the NaN-boxed label word of the neighbour
+    // same, with x = the NaN-boxed label word of the neighbour.  Branch-free:
+    // the sums that do not take this entry add +0.0, which leaves them
+    // bit-identical (they are never -0.0: they start at +0.0 and a sum that
+    // cancels to zero rounds to +0.0), so the four dependent chains pipeline.
     __device__ inline void add_boxed(double w, double x, double fu) {
+        const bool gt = is_boxed(x);
+        const int cls = boxed_class(x);
+        const double p = __dmul_rn(__dsub_rn(x, fu), w);
         w_all = __dadd_rn(w_all, w);
-        if (is_boxed(x)) {
-            if (boxed_class(x) == 0)
-                w0 = __dadd_rn(w0, w);
-            else
-                w1 = __dadd_rn(w1, w);
-        } else {
-            s = __dadd_rn(s, __dmul_rn(__dsub_rn(x, fu), w));
-        }
+        w0 = __dadd_rn(w0, (gt && cls == 0) ? w : 0.0);
+        w1 = __dadd_rn(w1, (gt && cls == 1) ? w : 0.0);
+        s = __dadd_rn(s, gt ? 0.0 : p);
     }
     // returns |fn - fu| or -1 for the isolated sentinel (value 0.5)
     __device__ inline double finish(double fu, double* out_val) const {

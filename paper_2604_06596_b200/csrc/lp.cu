@@ -51,10 +51,19 @@ namespace cg = cooperative_groups;
 namespace dlp {
 
 constexpr int kLpThreads = 256;
-constexpr int kWin = 64;        // row entries per warp window
-constexpr int kHubWin = 256;    // row entries per CTA window (hub rows)
+#ifndef DLP_WIN
+#define DLP_WIN 64
+#endif
+#ifndef DLP_HUB_WIN
+#define DLP_HUB_WIN 256
+#endif
+#ifndef DLP_LP_MINB
+#define DLP_LP_MINB 3
+#endif
+constexpr int kWin = DLP_WIN;   // row entries per warp window
+constexpr int kHubWin = DLP_HUB_WIN;  // row entries per CTA window (hub rows)
 constexpr int kLongRow = 96;    // rows longer than this are warp tiles of their own
-constexpr int kHubRow = 1024;   // rows longer than this are evaluated by a whole CTA
+constexpr int kHubRow = 384;    // rows longer than this are evaluated by a whole CTA
 constexpr int kScanRatio = 64;  // rounds with >= n/64 rows expand by atomicOr + compaction
 
 enum { PH_FRONTIER = 0, PH_DONE = 2 };
@@ -66,6 +75,11 @@ __constant__ int c_hub_row = kHubRow;
 __device__ inline int row_class(int len) {
     return len > c_hub_row ? CLS_HUB : (len > c_long_row ? CLS_LONG : CLS_SHORT);
 }
+// The prologue stores each eligible vertex's row class in bits 24-25 of its
+// eligibility word (column bits stay in 0-15), so claims and compaction get
+// the class from the word they already read.
+constexpr int kClassShift = 24;
+__device__ inline int elig_class(unsigned int e) { return (int)((e >> kClassShift) & 3u); }
 
 struct LPParams {
     const long long* row_start;
@@ -166,7 +180,8 @@ struct ClaimCtx {
 // append-mode claim: add v (for the columns in `bits` where it is eligible)
 // to the next union frontier; the first claimer appends it to its class list
 __device__ inline void claim(ClaimCtx& k, int v, unsigned int bits) {
-    bits &= k.eligm[v];
+    const unsigned int e = k.eligm[v];
+    bits &= e;
     if (!bits) return;
     k.claimed |= bits;
     unsigned int* fm = k.fm_next + v;
@@ -174,7 +189,7 @@ __device__ inline void claim(ClaimCtx& k, int v, unsigned int bits) {
     if ((cur & bits) == bits) return;
     unsigned int old = atomicOr(fm, bits);
     if (old != 0) return;
-    int cls = row_class(k.row_len[v]);
+    const int cls = elig_class(e);
     if (cls == CLS_SHORT)
         append_u32(k.next[0], &k.cnt[0], v);
     else if (cls == CLS_LONG)
@@ -524,7 +539,7 @@ __device__ void cta_hub_row(const LPParams& P, const RoundCtx& R, ClaimCtx& K, B
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(kLpThreads, 2) k_lp_fused(LPParams P) {
+__global__ void __launch_bounds__(kLpThreads, DLP_LP_MINB) k_lp_fused(LPParams P) {
     extern __shared__ double smem_dyn[];
     __shared__ ColState S;
     __shared__ BlockCounters B;
@@ -570,7 +585,9 @@ __global__ void __launch_bounds__(kLpThreads, 2) k_lp_fused(LPParams P) {
     }
     for (long long i = gtid; i < n_el; i += gth) {
         int u = P.elist[i];
-        switch (row_class(P.row_len[u])) {
+        const int cls = row_class(P.row_len[u]);
+        P.eligm[u] |= (unsigned int)cls << kClassShift;
+        switch (cls) {
             case CLS_SHORT: append_u32(P.elist_c[0], &ctl->n_el[0], u); break;
             case CLS_LONG: append_u32(P.elist_c[1], &ctl->n_el[1], u); break;
             default: append_u32(P.elist_c[2], &ctl->n_el[2], u); break;
@@ -693,15 +710,18 @@ __global__ void __launch_bounds__(kLpThreads, 2) k_lp_fused(LPParams P) {
             // issues a single atomic per list
             const long long chunk = ((n + gridDim.x - 1) / gridDim.x + 255) & ~255LL;
             const long long v0 = blockIdx.x * chunk, v1 = min(n, v0 + chunk);
+            // pass 1 (independent coalesced loads, unrolled): drop ineligible
+            // claims, count per class
             unsigned int cc[3] = {0u, 0u, 0u};
+#pragma unroll 4
             for (long long v = v0 + tid; v < v1; v += kLpThreads) {
-                unsigned int bits = fm_next[v];
+                const unsigned int bits = fm_next[v], e = P.eligm[v];
                 if (!bits) continue;
-                if (!(bits & P.eligm[v])) {
+                if (!(bits & e)) {
                     fm_next[v] = 0;  // claimed but ineligible: never evaluated
                     continue;
                 }
-                int cls = row_class(P.row_len[v]);
+                const int cls = elig_class(e);
                 cc[0] += cls == 0;
                 cc[1] += cls == 1;
                 cc[2] += cls == 2;
@@ -721,19 +741,23 @@ __global__ void __launch_bounds__(kLpThreads, 2) k_lp_fused(LPParams P) {
                 s_base[tid] = tot ? atomicAdd(&slot->cnt[tid], tot) : 0u;
             }
             __syncthreads();
+            // pass 2 (L1-resident re-read): write the class lists
+            const unsigned int below = (1u << lane) - 1u;
+            unsigned int off0 = s_base[0] + s_wc[0][warp], off1 = s_base[1] + s_wc[1][warp],
+                         off2 = s_base[2] + s_wc[2][warp];
             for (long long vb = v0; vb < v1; vb += kLpThreads) {
-                long long v = vb + tid;
-                unsigned int bits = v < v1 ? fm_next[v] : 0u;
-                int cls = bits ? row_class(P.row_len[v]) : -1;
-                const unsigned int below = (1u << lane) - 1u;
-#pragma unroll
-                for (int j = 0; j < 3; j++) {
-                    unsigned int bj = __ballot_sync(0xffffffffu, cls == j);
-                    if (cls == j) P.flist[j][rn][s_base[j] + s_wc[j][warp] + __popc(bj & below)] = (int)v;
-                    __syncwarp();
-                    if (lane == 0) s_wc[j][warp] += __popc(bj);
-                    __syncwarp();
-                }
+                const long long v = vb + tid;
+                const unsigned int bits = v < v1 ? fm_next[v] : 0u;
+                const int cls = bits ? elig_class(P.eligm[v]) : -1;
+                const unsigned int b0 = __ballot_sync(0xffffffffu, cls == 0);
+                const unsigned int b1 = __ballot_sync(0xffffffffu, cls == 1);
+                const unsigned int b2 = __ballot_sync(0xffffffffu, cls == 2);
+                if (cls == 0) P.flist[0][rn][off0 + __popc(b0 & below)] = (int)v;
+                if (cls == 1) P.flist[1][rn][off1 + __popc(b1 & below)] = (int)v;
+                if (cls == 2) P.flist[2][rn][off2 + __popc(b2 & below)] = (int)v;
+                off0 += __popc(b0);
+                off1 += __popc(b1);
+                off2 += __popc(b2);
             }
         }
         if (gtid == 0) {
@@ -804,7 +828,8 @@ __global__ void __launch_bounds__(kLpThreads, 2) k_lp_fused(LPParams P) {
 void lp_setup(Engine& E) {
     if (E.lp_grid) return;
     if (E.ncol > kMaxCols) throw CudaFailure(cudaErrorInvalidValue, "ncol > kMaxCols", __FILE__, __LINE__);
-    E.lp_smem = (size_t)(kLpThreads / 32) * (kWin * (E.ncol + 1) + 32) * sizeof(double);
+    E.lp_smem = std::max((size_t)(kLpThreads / 32) * (kWin * (E.ncol + 1) + 32),
+                         (size_t)2 * kHubWin * (E.ncol + 1)) * sizeof(double);
     DLP_CUDA_TRY(cudaFuncSetAttribute(k_lp_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)E.lp_smem));
     int occ = 0;
     DLP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_lp_fused, kLpThreads, E.lp_smem));
