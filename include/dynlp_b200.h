@@ -152,6 +152,31 @@ int dlp_jacobi_run(const int64_t* indptr, const int64_t* indices, const double* 
                    int64_t* out_warnings, int64_t* leftover, int64_t* n_leftover);
 const char* dlp_plugin_last_error(void);
 
+/* ---- k-NN edge construction (builder.py:18-92) -------------------------
+ * Cosine k-NN on tensor cores (fp16 hi/lo split, fp32 accumulation in TMEM)
+ * with an exact fp64 re-check and certificate: the selected pairs are those
+ * of an exact fp64 selection by (-sim, id); weights are fp64 dot products. */
+typedef struct dlp_knn dlp_knn;
+int dlp_knn_create(int device, dlp_knn** out);
+int dlp_knn_destroy(dlp_knn* h);
+const char* dlp_knn_last_error(dlp_knn* h);
+/* FeatureMatrix (builder.py:18-39): HOST rows [n][d] fp64; all-zero rows are
+ * rejected (status 3, "all-zero feature row i (cosine undefined)"). */
+int dlp_knn_set_features(dlp_knn* h, const double* rows, int64_t n, int64_t d);
+/* top-k rows of queries [q0, q1) against all n rows (self excluded), each row
+ * ordered by (-sim, id): the k-NN rows of a batch of arriving points. */
+int dlp_knn_query(dlp_knn* h, int64_t q0, int64_t q1, int32_t k, int64_t* ids, double* sims);
+/* knn_graph (builder.py:42-92): union-symmetrised, max-merged, sorted by
+ * (lo, hi); affine = 0 for "prune" (w = cos), 1 for "affine" (w = (1+cos)/2). */
+int dlp_knn_graph(dlp_knn* h, int32_t k, int32_t affine, int64_t* m_out);
+int dlp_knn_read_edges(dlp_knn* h, int64_t* u, int64_t* v, double* w, int64_t m);
+/* timings (CUDA events) and certificate fallbacks of the last call */
+int dlp_knn_stats(dlp_knn* h, double* screen_ms, double* recheck_ms, double* exact_ms, int64_t* n_fallback,
+                  int64_t* n_queries, double* eps);
+/* screened candidates of the last dlp_knn_query (tests of the tensor-core stage) */
+int dlp_knn_debug_candidates(dlp_knn* h, int64_t q0, int64_t q1, int32_t* nsplit, float* val, int32_t* id,
+                             float* thr, int64_t cap);
+
 /* Device / build facts for reports: SM count and whether the sm_100a image
  * is loadable on the current device. */
 int dlp_device_info(int device, int* sm_count, int* cc_major, int* cc_minor);

@@ -71,6 +71,15 @@ SIGNATURES = {
     "dlp_jacobi_run": (_int, [_p, _p, _p, _p, _p, _i64, _p, _i64, _p, _dbl, _i64,
                               _p, _p, _p, _p, _p, _p]),
     "dlp_plugin_last_error": (C.c_char_p, []),
+    "dlp_knn_create": (_int, [_int, _p]),
+    "dlp_knn_destroy": (_int, [_p]),
+    "dlp_knn_last_error": (C.c_char_p, [_p]),
+    "dlp_knn_set_features": (_int, [_p, _p, _i64, _i64]),
+    "dlp_knn_query": (_int, [_p, _i64, _i64, _i32, _p, _p]),
+    "dlp_knn_graph": (_int, [_p, _i32, _i32, _p]),
+    "dlp_knn_read_edges": (_int, [_p, _p, _p, _p, _i64]),
+    "dlp_knn_stats": (_int, [_p, _p, _p, _p, _p, _p, _p]),
+    "dlp_knn_debug_candidates": (_int, [_p, _i64, _i64, _p, _p, _p, _p, _i64]),
     "dlp_device_info": (_int, [_int, _p, _p, _p]),
 }
 
