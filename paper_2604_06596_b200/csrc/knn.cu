@@ -13,9 +13,11 @@
 //   (np.linalg.norm(axis=1) = sqrt(add.reduce(x*x))), rows divided by them
 //   (IEEE division) -> the normalised fp64 rows the exact stage uses.  The same
 //   kernel emits the tensor-core operands: fp16 hi/lo split h = fp16(x),
-//   l = fp16(x - h), laid out along K as [h|h|l] for queries and [h|l|h] for
-//   the database so ONE fp32-accumulated GEMM of depth 3D yields
-//   h.h' + h.l' + l.h' (error ~1e-6 instead of ~1e-3 for a single fp16 pass).
+//   l = fp16(x - h), laid out along K as [h|l] for both operands; the MMA
+//   issuer pairs K steps so ONE fp32 accumulator receives h.h' + l.h' + h.l'
+//   (error ~1e-6 instead of ~1e-3 for a single fp16 pass) while the
+//   streamed database operand is only 2D wide (each database h slab feeds
+//   two MMAs).
 //   Operands are stored pre-swizzled in the UMMA SWIZZLE_128B K-major layout,
 //   so plain bulk copies (cp.async.bulk, SASS UBLKCP) land them ready for
 //   tcgen05.mma.
@@ -97,9 +99,12 @@ __host__ __device__ inline size_t sw128_off(long long row, int kk, int R, int KB
     return (((size_t)tile * KB + kb) * R + rr) * 128 + (size_t)((c ^ (rr & 7)) << 4) + (size_t)(e << 1);
 }
 
-// thread per row: norm, normalised fp64 row, fp16 split operands
-__global__ void k_knn_norm(const double* x, long long n, int D, int KB, double* xn, __half* opA, __half* opB,
-                           long long* bad_row) {
+// thread per row: norm, normalised fp64 row, fp16 split operands.  Both
+// operands hold [h | l] along K (h at K steps [0, Dp/16), l at [Dp/16, 2Dp/16),
+// Dp = D rounded up to the MMA K of 16, zero padded); the screen issues
+// h.h' + l.h' for the database's h steps and h.l' for its l steps.
+__global__ void k_knn_norm(const double* x, long long n, int D, int Dp, int KB, double* xn, __half* opA,
+                           __half* opB, long long* bad_row) {
     for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x) {
         const double* row = x + r * D;
         double nrm = __dsqrt_rn(pw_sum_sq(row, D, 1));
@@ -112,16 +117,10 @@ __global__ void k_knn_norm(const double* x, long long n, int D, int KB, double* 
             xn[r * D + d] = v;
             __half h = __double2half(v);
             __half l = __double2half(__dsub_rn(v, (double)__half2float(h)));
-            if (opA) {  // queries: [h | h | l]
-                opA[sw128_off(r, d, BM, KB) / 2] = h;
-                opA[sw128_off(r, D + d, BM, KB) / 2] = h;
-                opA[sw128_off(r, 2 * D + d, BM, KB) / 2] = l;
-            }
-            if (opB) {  // database: [h | l | h]
-                opB[sw128_off(r, d, BN, KB) / 2] = h;
-                opB[sw128_off(r, D + d, BN, KB) / 2] = l;
-                opB[sw128_off(r, 2 * D + d, BN, KB) / 2] = h;
-            }
+            opA[sw128_off(r, d, BM, KB) / 2] = h;
+            opA[sw128_off(r, Dp + d, BM, KB) / 2] = l;
+            opB[sw128_off(r, d, BN, KB) / 2] = h;
+            opB[sw128_off(r, Dp + d, BN, KB) / 2] = l;
         }
     }
 }
@@ -195,10 +194,35 @@ __host__ __device__ constexpr unsigned int f16_idesc(int M, int N) {
           "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])                 \
         : "r"(taddr))
 
+// sift-down of a KP-entry min-heap stored as lv/li[slot * BM + et]
+__device__ inline void heap_sift(float* lv, int* li, int et, int i) {
+    float v = lv[i * BM + et];
+    int id = li[i * BM + et];
+    for (;;) {
+        int c = 2 * i + 1;
+        if (c >= KP) break;
+        float cv = lv[c * BM + et];
+        if (c + 1 < KP) {
+            float c2 = lv[(c + 1) * BM + et];
+            if (c2 < cv) {
+                cv = c2;
+                c++;
+            }
+        }
+        if (!(cv < v)) break;
+        lv[i * BM + et] = cv;
+        li[i * BM + et] = li[c * BM + et];
+        i = c;
+    }
+    lv[i * BM + et] = v;
+    li[i * BM + et] = id;
+}
+
 struct ScreenArgs {
     const unsigned char* opA;  // query operand (pre-swizzled), tiles of BM rows
     const unsigned char* opB;  // database operand, tiles of BN rows
-    int KB;                    // K blocks (3D padded to 64)
+    int KB;                    // K blocks of [h | l] (2*Dp padded to 64)
+    int hsteps;                // Dp / 16: K steps of the h half
     long long q0, nq;          // global id of query row 0 of opA, query count
     long long n_db;            // database rows
     int n_btiles;              // database tiles of BN rows
@@ -216,7 +240,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_knn_screen(ScreenArgs a) {
     unsigned char* sB = sA + (size_t)a.KB * A_BLOCK;
     float* lv = (float*)(sB + (size_t)a.stages * B_BLOCK);  // [KP][128]
     int* li = (int*)(lv + KP * BM);                         // [KP][128]
-    unsigned long long* bars = (unsigned long long*)(li + KP * BM);
+    float* pv = (float*)(li + KP * BM);                     // pending [32][128]
+    int* pi = (int*)(pv + 32 * BM);                         // pending ids
+    unsigned long long* bars = (unsigned long long*)(pi + 32 * BM);
     unsigned long long* full = bars;                     // [stages]
     unsigned long long* empty = bars + a.stages;         // [stages]
     unsigned long long* tfull = bars + 2 * a.stages;     // [2]
@@ -287,14 +313,26 @@ __global__ void __launch_bounds__(kThreads, 1) k_knn_screen(ScreenArgs a) {
                 mbar_wait(&tempty[acc], accph ^ 1);
                 tc_fence_after();
                 const unsigned int dtm = tmem + (unsigned int)(acc * BN);
+                const unsigned int sa0 = smem_u32(sA);
+                unsigned int accum = 0;
                 for (int kb = 0; kb < a.KB; kb++) {
                     mbar_wait(&full[st], ph);
                     tc_fence_after();
-                    const unsigned int sa = smem_u32(sA + (size_t)kb * A_BLOCK);
                     const unsigned int sb = smem_u32(sB + (size_t)st * B_BLOCK);
 #pragma unroll
-                    for (int k = 0; k < BKH / 16; k++)
-                        tc_mma(dtm, sw128_desc(sa + k * 32), sw128_desc(sb + k * 32), idesc, (kb | k) != 0);
+                    for (int k = 0; k < BKH / 16; k++) {
+                        const int gs = kb * (BKH / 16) + k;  // database K step
+                        const unsigned long long bd = sw128_desc(sb + k * 32);
+                        if (gs < a.hsteps) {  // database h: query h and query l
+                            const int qa = gs, ql = gs + a.hsteps;
+                            tc_mma(dtm, sw128_desc(sa0 + (qa >> 2) * A_BLOCK + (qa & 3) * 32), bd, idesc, accum);
+                            accum = 1;
+                            tc_mma(dtm, sw128_desc(sa0 + (ql >> 2) * A_BLOCK + (ql & 3) * 32), bd, idesc, 1);
+                        } else if (gs < 2 * a.hsteps) {  // database l: query h
+                            const int qa = gs - a.hsteps;
+                            tc_mma(dtm, sw128_desc(sa0 + (qa >> 2) * A_BLOCK + (qa & 3) * 32), bd, idesc, 1);
+                        }
+                    }
                     tc_commit(&empty[st]);  // frees the stage once these MMAs complete
                     if (++st == a.stages) {
                         st = 0;
@@ -320,8 +358,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_knn_screen(ScreenArgs a) {
             const int t0 = split * a.tiles_per_split, t1 = min(a.n_btiles, t0 + a.tiles_per_split);
             const long long qrow = (long long)qt * BM + et;
             const long long qid = a.q0 + qrow;
+            // per-query top-KP as a min-heap in shared memory ([slot][lane]
+            // layout, conflict-free), thr = its root.  A chunk's values above
+            // thr are first appended (predicated, no divergence) to a pending
+            // list, then merged into the heap by all lanes in lockstep.
             float thr = -INFINITY;
-            int cnt = 0, pos = 0;
+            int cnt = 0;
             for (int t = t0; t < t1; t++) {
                 mbar_wait(&tfull[acc], accph);
                 tc_fence_after();
@@ -330,33 +372,38 @@ __global__ void __launch_bounds__(kThreads, 1) k_knn_screen(ScreenArgs a) {
                     TMEM_LD32(tmem + lane_base + (unsigned int)(acc * BN + j * 32), r);
                     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                     const long long g0 = (long long)t * BN + j * 32;
+                    float mx = __uint_as_float(r[0]);
+#pragma unroll
+                    for (int c = 1; c < 32; c++) mx = fmaxf(mx, __uint_as_float(r[c]));
+                    const bool special = (qid >= g0 && qid < g0 + 32) || g0 + 32 > a.n_db;
+                    if (!__any_sync(0xffffffffu, mx > thr || special)) continue;
+                    int pc = 0;
 #pragma unroll
                     for (int c = 0; c < 32; c++) {
                         const float v = __uint_as_float(r[c]);
                         const long long gid = g0 + c;
-                        if (!(v > thr) || gid >= a.n_db || gid == qid) continue;
+                        const bool pass = v > thr && gid < a.n_db && gid != qid;
+                        if (pass) {
+                            pv[pc * BM + et] = v;
+                            pi[pc * BM + et] = (int)gid;
+                        }
+                        pc += pass ? 1 : 0;
+                    }
+                    for (int p = 0; p < pc; p++) {
+                        const float v = pv[p * BM + et];
+                        const int gid = pi[p * BM + et];
                         if (cnt < KP) {
                             lv[cnt * BM + et] = v;
-                            li[cnt * BM + et] = (int)gid;
-                            if (++cnt == KP) {  // list full: threshold = its minimum
+                            li[cnt * BM + et] = gid;
+                            if (++cnt == KP) {  // heapify once the list is full
+                                for (int i0 = KP / 2 - 1; i0 >= 0; i0--) heap_sift(lv, li, et, i0);
                                 thr = lv[et];
-                                pos = 0;
-                                for (int s = 1; s < KP; s++)
-                                    if (lv[s * BM + et] < thr) {
-                                        thr = lv[s * BM + et];
-                                        pos = s;
-                                    }
                             }
-                        } else {
-                            lv[pos * BM + et] = v;
-                            li[pos * BM + et] = (int)gid;
+                        } else if (v > thr) {  // replace the root, restore the heap
+                            lv[et] = v;
+                            li[et] = gid;
+                            heap_sift(lv, li, et, 0);
                             thr = lv[et];
-                            pos = 0;
-                            for (int s = 1; s < KP; s++)
-                                if (lv[s * BM + et] < thr) {
-                                    thr = lv[s * BM + et];
-                                    pos = s;
-                                }
                         }
                     }
                 }
@@ -589,7 +636,7 @@ struct dlp_knn {
     int sm_count = 148;
     std::string err;
     long long n = 0;
-    int D = 0, KB = 0;
+    int D = 0, Dp = 0, KB = 0;
     DevArray<double> x, xn;
     DevArray<unsigned char> opA, opB;  // query operand covers all rows (queries are row ranges)
     DevArray<float> cand_val, cand_min;
@@ -614,6 +661,26 @@ struct dlp_knn {
 
 namespace {
 
+// database splits per query tile: enough (query tile, split) items to fill
+// every SM, chosen to minimise the last-wave idle fraction
+int choose_nsplit(int nqt, int n_btiles, int sms) {
+    int best = 1;
+    double best_eff = -1.0;
+    for (int s = 1; s <= std::min(16, n_btiles); s++) {
+        const int tps = (n_btiles + s - 1) / s;
+        const int sp = (n_btiles + tps - 1) / tps;
+        const long long items = (long long)nqt * sp;
+        const long long waves = (items + sms - 1) / sms;
+        double eff = (double)items / (double)(waves * sms);
+        if (items < sms) eff *= 0.5;  // under-filled grid
+        if (eff > best_eff + 1e-9) {
+            best_eff = eff;
+            best = s;
+        }
+    }
+    return best;
+}
+
 int kfail(dlp_knn* h, int code, const char* msg) {
     h->err = msg;
     return code;
@@ -623,7 +690,7 @@ int kfail(dlp_knn* h, int code, const char* msg) {
 // dropped l.l' and second-order rounding terms, plus fp32 accumulation of
 // 3D exact fp16 products (2^-23 relative per addition, partial sums <= ~1.02)
 double screen_eps(int D) {
-    double k3 = 3.0 * D;
+    double k3 = 3.0 * ((D + 15) / 16 * 16);
     return k3 * std::ldexp(1.0, -23) * 1.02 + std::ldexp(1.0, -20) + 2.0 * std::ldexp(1.0, -25) * std::sqrt((double)D) +
            std::ldexp(1.0, -21) + 1e-12;
 }
@@ -644,8 +711,7 @@ int run_queries(dlp_knn* h, long long q0, long long nq, int k) {
         // --- screen: (query tile, database split) work items over all SMs
         const int nqt = (int)((nq + BM - 1) / BM);
         const int n_btiles = (int)((n + BN - 1) / BN);
-        int nsplit = std::max(1, (2 * h->sm_count + nqt - 1) / nqt);
-        nsplit = std::min(nsplit, std::min(16, n_btiles));
+        int nsplit = choose_nsplit(nqt, n_btiles, h->sm_count);
         const int tps = (n_btiles + nsplit - 1) / nsplit;
         nsplit = (n_btiles + tps - 1) / tps;
         h->cand_val.reserve((size_t)nq * nsplit * KP, 0, st);
@@ -655,6 +721,7 @@ int run_queries(dlp_knn* h, long long q0, long long nq, int k) {
         a.opA = h->opA.p + (size_t)(q0 / BM) * h->KB * A_BLOCK;
         a.opB = h->opB.p;
         a.KB = h->KB;
+        a.hsteps = h->Dp / 16;
         a.q0 = (q0 / BM) * BM;  // screening works on whole query tiles
         long long qpad = q0 - a.q0;
         a.nq = nq + qpad;
@@ -663,9 +730,9 @@ int run_queries(dlp_knn* h, long long q0, long long nq, int k) {
         a.nsplit = nsplit;
         a.tiles_per_split = tps;
         a.nqt = (int)((a.nq + BM - 1) / BM);
-        const size_t fixed = (size_t)h->KB * A_BLOCK + (size_t)KP * BM * 8 + 1024 + 256;
+        const size_t fixed = (size_t)h->KB * A_BLOCK + (size_t)(KP + 32) * BM * 8 + 1024 + 256;
         const size_t limit = 227 * 1024;
-        a.stages = (int)std::min<size_t>(4, (limit - fixed) / B_BLOCK);
+        a.stages = (int)std::min<size_t>(8, (limit - fixed) / B_BLOCK);
         if (a.stages < 2) return kfail(h, DLP_EVALIDATION, "feature dimension too large for the tensor-core screen");
         // candidate buffers are indexed by the padded query row
         h->cand_val.reserve((size_t)a.nq * nsplit * KP, 0, st);
@@ -799,7 +866,8 @@ int dlp_knn_set_features(dlp_knn* h, const double* rows, int64_t n, int64_t d) {
         DLP_CUDA_TRY(cudaSetDevice(h->device));
         cudaStream_t st = h->st;
         const int D = (int)d;
-        const int KB = (3 * D + BKH - 1) / BKH;
+        const int Dp = (D + 15) / 16 * 16;
+        const int KB = (2 * Dp + BKH - 1) / BKH;
         h->x.reserve((size_t)n * D, 0, st);
         h->xn.reserve((size_t)n * D, 0, st);
         DLP_CUDA_TRY(cudaMemcpyAsync(h->x.p, rows, (size_t)n * D * sizeof(double), cudaMemcpyHostToDevice, st));
@@ -812,7 +880,7 @@ int dlp_knn_set_features(dlp_knn* h, const double* rows, int64_t n, int64_t d) {
         h->bad.reserve(1, 0, st);
         long long big = 0x7fffffffffffffffLL;
         DLP_CUDA_TRY(cudaMemcpyAsync(h->bad.p, &big, sizeof(big), cudaMemcpyHostToDevice, st));
-        k_knn_norm<<<blocks_for(n, 128, 148 * 32), 128, 0, st>>>(h->x.p, n, D, KB, h->xn.p, (__half*)h->opA.p,
+        k_knn_norm<<<blocks_for(n, 128, 148 * 32), 128, 0, st>>>(h->x.p, n, D, Dp, KB, h->xn.p, (__half*)h->opA.p,
                                                                  (__half*)h->opB.p, h->bad.p);
         DLP_CUDA_TRY(cudaGetLastError());
         long long bad = 0;
@@ -827,6 +895,7 @@ int dlp_knn_set_features(dlp_knn* h, const double* rows, int64_t n, int64_t d) {
         h->n = n;
         h->D = D;
         h->KB = KB;
+        h->Dp = Dp;
         h->eps = screen_eps(D);
     } catch (const CudaFailure& f) {
         h->err = std::string("CUDA error: ") + cudaGetErrorString(f.err);
@@ -985,8 +1054,7 @@ int dlp_knn_debug_candidates(dlp_knn* h, int64_t q0, int64_t q1, int32_t* nsplit
         const long long nq = q1 - q0;
         const int nqt = (int)((nq + BM - 1) / BM);
         const int n_btiles = (int)((h->n + BN - 1) / BN);
-        int nsplit = std::max(1, (2 * h->sm_count + nqt - 1) / nqt);
-        nsplit = std::min(nsplit, std::min(16, n_btiles));
+        int nsplit = choose_nsplit(nqt, n_btiles, h->sm_count);
         const int tps = (n_btiles + nsplit - 1) / nsplit;
         nsplit = (n_btiles + tps - 1) / tps;
         *nsplit_out = nsplit;
