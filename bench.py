@@ -68,7 +68,7 @@ def make_stream(cfg, device):
     os.makedirs(cache_dir, exist_ok=True)
     key = "_".join(str(cfg[k]) for k in ("n", "dim", "classes", "k", "seed_frac", "batch", "seed")) + \
         "_" + "_".join(str(x) for x in cfg["fractions"])
-    path = os.path.join(cache_dir, f"stream_{key}.npz")
+    path = os.path.join(cache_dir, f"stream_{key}_exactknn.npz")
     if os.path.exists(path):
         z = np.load(path)
         from paper_2604_06596_b200.batch import BatchUpdate
@@ -80,14 +80,17 @@ def make_stream(cfg, device):
                    for t in range(len(io) - 1)]
         return batches, z["classes"]
     t0 = time.time()
-    bl = streams.make_blobs(cfg["n"], cfg["dim"], cfg["classes"], cfg["seed"], dtype=np.float32)
-    if device is not None and cfg["n"] > 20_000:
-        import torch
+    bl = streams.make_blobs(cfg["n"], cfg["dim"], cfg["classes"], cfg["seed"])
+    if device is not None:
+        # the B200 k-NN builder (knn.py: tensor-core screen + exact fp64 re-check):
+        # the same edge set as the reference's knn_graph (builder.py:42-92)
+        from paper_2604_06596_b200.knn import KnnIndex
 
-        torch.backends.cuda.matmul.allow_tf32 = True
-        edges = streams.knn_graph_torch(bl.x, cfg["k"], device=device, block=4096)
+        idx = KnnIndex(bl.x, int(device.split(":")[-1]))
+        edges = idx.graph(cfg["k"])
+        idx.close()
     else:
-        edges = streams.knn_graph_exact(bl.x.astype(np.float64), cfg["k"])
+        edges = streams.knn_graph_exact(bl.x, cfg["k"])
     gt = streams.stratified_seeds(bl.classes, cfg["seed_frac"], cfg["seed"])
     fi, fg, fd = cfg["fractions"]
     if fd > 0:
@@ -212,6 +215,48 @@ def cpu_reference_run(batches, t0, steps, F0, ncol, delta, threads, column=0, ki
     return "port", times, reps
 
 
+def knn_leg(cfg, batches, device_index, K):
+    """Per-batch k-NN edge construction: the arriving points
+    of the last timed batch queried against all N points, on tensor cores."""
+    from paper_2604_06596_b200 import streams
+    from paper_2604_06596_b200.knn import KnnIndex
+
+    bl = streams.make_blobs(cfg["n"], cfg["dim"], cfg["classes"], cfg["seed"])
+    idx = KnnIndex(bl.x, device_index)
+    q = cfg["batch"]
+    runs = []
+    for r in range(max(3, min(K, 5)) + 1):
+        q0 = cfg["n"] - q * (r % 3 + 1)
+        s = time.perf_counter()
+        idx.query(q0, q0 + q, cfg["k"])
+        wall = (time.perf_counter() - s) * 1e3
+        st = idx.stats()
+        if r:  # first call is a warm-up
+            runs.append((wall, st.screen_ms, st.recheck_ms, st.exact_ms, st.fallback_queries))
+    idx.close()
+    wall, scr, rec, ex, fb = (float(np.median([x[i] for x in runs])) for i in range(5))
+    kext = 3 * ((cfg["dim"] + 15) // 16 * 16)  # three Dp-deep fp16 products per pair
+    flops_alg = 2.0 * q * cfg["n"] * cfg["dim"]
+    flops_exec = 2.0 * q * cfg["n"] * kext
+    peak = measured_tensor_peak()
+    return {"queries": q, "points": cfg["n"], "dim": cfg["dim"], "k": cfg["k"],
+            "ms": wall, "screen_ms": scr, "recheck_ms": rec, "exact_fallback_ms": ex,
+            "fallback_queries": fb,
+            "roofline": {"bound": "tensor", "achieved": flops_exec / (scr * 1e-3) / 1e12, "peak": peak,
+                         "unit": "TFLOP/s", "frac": flops_exec / (scr * 1e-3) / 1e12 / peak,
+                         "algorithmic_tflops": flops_alg / (scr * 1e-3) / 1e12,
+                         "note": "executed = 3 fp16 products (hi/lo split) per pair; algorithmic = 2QND; "
+                                 "peak = MEASURED_PEAKS.json bf16_tflops (dense fp16 == bf16 rate)",
+                         "kernel": "k_knn_screen (tcgen05.mma kind::f16, TMEM accumulators)"}}
+
+
+def measured_tensor_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        return float(json.load(open(p))["bf16_tflops"])
+    return 1590.0
+
+
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -239,6 +284,8 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--n", type=int, default=None, help="override point count (smaller smoke runs)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-knn", action="store_true", help="skip the k-NN edge-construction leg")
+    ap.add_argument("--replicas", action="store_true", help="N > 1: independent replicas instead of sharding")
     ap.add_argument("--cpu-kind", default=None, choices=[None, "reference", "port"])
     args = ap.parse_args()
 
@@ -257,11 +304,15 @@ def main():
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl" if have_gpu else "gloo")
+        # DYNLP_BENCH_BACKEND=gloo + DYNLP_BENCH_ONE_DEVICE=1: exercise the multi-rank
+        # path with every rank on GPU 0 (protocol checks on a one-GPU box)
+        dist.init_process_group(os.environ.get("DYNLP_BENCH_BACKEND", "nccl" if have_gpu else "gloo"))
     if args.impl == "reference" and rank != 0:
         if dist:
             dist.destroy_process_group()
         return
+    if os.environ.get("DYNLP_BENCH_ONE_DEVICE"):
+        local = 0
     device = f"cuda:{local}" if have_gpu else None
     if have_gpu:
         torch.cuda.set_device(local)
@@ -283,15 +334,35 @@ def main():
     ecfg = EngineConfig(delta=delta)
     threads = os.cpu_count() or 1
 
+    # N > 1: one C2 stream, connected components sharded over the ranks
+    # (sharded.py; phase bookkeeping reduced with NCCL); --replicas runs N
+    # independent copies instead.
+    sharded = world > 1 and not args.replicas
+    if sharded:
+        from paper_2604_06596_b200.sharded import ShardedGraph, apply_batch_sharded, torch_collective
+
+        nccl = dist.get_backend() == "nccl"
+        coll = torch_collective(device=device if nccl else None)
+
+    def new_graph():
+        if sharded:
+            return ShardedGraph(local, max(2, cfg["classes"]), rank, world, coll), LabelState()
+        return DynamicGraph(local, num_classes=max(2, cfg["classes"])), LabelState()
+
+    def step(g, lab, b):
+        if sharded:
+            return apply_batch_sharded(g, lab, b, ecfg)
+        return apply_batch(g, lab, b, ecfg)
+
     def bootstrap():
-        g, lab = DynamicGraph(local, num_classes=max(2, cfg["classes"])), LabelState()
+        g, lab = new_graph()
         # capacity hint for the whole stream (setup, untimed): no reallocation in timed steps
         g.reserve(sum(len(b.insert_ids) for b in batches), sum(len(b.edge_owner) for b in batches))
         s = time.time()
         for b in batches[:tw]:
-            apply_batch(g, lab, b, ecfg)
+            step(g, lab, b)
         for b in batches[tw:t0]:  # warm-up steps (untimed)
-            apply_batch(g, lab, b, ecfg)
+            step(g, lab, b)
         log(f"[bench] rank {rank}: bootstrap+warmup {t0} batches in {time.time() - s:.1f}s, |V|={g.num_slots}")
         return g, lab
 
@@ -352,7 +423,11 @@ def main():
     ev0.record()
     repsA = []
     for s in range(K):
-        repsA.append(gA.apply_device(dev[s], ecfg, trusted=True))
+        if sharded:  # sharded batches enter through the host path on every rank
+            r = step(gA, labA, batches[t0 + s])[1]
+            repsA.append(r if isinstance(r, list) else [r])
+        else:
+            repsA.append(gA.apply_device(dev[s], ecfg, trusted=True))
     ev1.record()
     barrier()
     clk = clocks.stop()
@@ -368,7 +443,7 @@ def main():
     ev0.record()
     repsB = []
     for b in batches[t0:]:
-        labB, r = apply_batch(gB, labB, b, ecfg)
+        labB, r = step(gB, labB, b)
         repsB.append(r if isinstance(r, list) else [r])
         d2h = ctypes_report_bytes(ncol)
     ev1.record()
@@ -389,7 +464,7 @@ def main():
     # label vector; per (vertex, column) update 8 B f read + 8 B staged write +
     # 8 B staged read + 8 B commit write.
     alg_bytes = 20.0 * urows + (12.0 + 8.0 * ncol) * uent + 32.0 * upd
-    achieved = alg_bytes / (lp_ms * 1e-3) / 1e9 if lp_ms > 0 else None
+    achieved = alg_bytes / (lp_ms * 1e-3) / 1e9 if lp_ms > 0 and uent > 0 else None
     survey_bytes = 32.0 * upd + 21.0 * edges  # SURVEY §8(d) D-4 per-column model
     peak, peak_kind = measured_peaks()
     tr = traffic_record()
@@ -397,10 +472,13 @@ def main():
                for a, b in zip(repsA, repsB) for c in range(len(a)))
     line = {
         "metric": "dynlp_ms_per_batch", "value": ms_value, "unit": "ms/batch", "n_gpus": world,
-        "steps": K, "warmup": W, "ms_per_step": ms_value, "higher_is_better": False, "scaling": "weak",
+        "steps": K, "warmup": W, "ms_per_step": ms_value, "higher_is_better": False,
+        "scaling": "strong" if sharded else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": cfg["desc"], "points": cfg["n"], "timed_batches": f"t={t0}..{T - 1}",
-                   "label_columns": ncol, "delta": delta, "parallelism": f"replicas x{world}",
+                   "label_columns": ncol, "delta": delta,
+                   "parallelism": (f"component-sharded x{world} (NCCL phase all-reduce)" if sharded
+                                   else f"replicas x{world}"),
                    "l2": "no flush: per-batch working set (adjacency ~200 MB + 10 label columns) exceeds "
                          "the 126 MB L2"},
         "edges_per_s": edges / (ms_value * K * 1e-3),
@@ -425,6 +503,8 @@ def main():
         "certify_sweeps_per_batch": sum(r.certify_sweeps for step in repsA for r in step) / K,
         "legs_identical_work": same,
     }
+    if rank == 0 and not args.no_knn:
+        line["knn"] = knn_leg(cfg, batches, local, K)
     if rank == 0 and not args.no_cpu_baseline:
         kind, times, reps = cpu_reference_run(batches, t0, 1, F0, ncol, delta, threads, kind=args.cpu_kind)
         gpu_col0 = repsA[0][0]

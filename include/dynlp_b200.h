@@ -113,6 +113,22 @@ int dlp_itlp_batch(dlp_engine* e, const dlp_config* cfg, const dlp_batch* batch,
  * later batches never reallocate.  Optional; growth is otherwise geometric. */
 int dlp_reserve(dlp_engine* e, int64_t n_vertices, int64_t n_edges);
 
+/* ---- component sharding ------------------------------
+ * Every rank applies the same batches (replicated structure, tau, components,
+ * initialisation); each rank propagates only the connected components it
+ * owns (a hash of the component's minimum vertex id).  The per-column
+ * frontier / certify state machine of engine.py:375-405 runs on phase
+ * results reduced over all ranks through the caller's collective: `reduce`
+ * must combine imax (elementwise max), isum (sum) and dmax (max) in place
+ * across ranks and return 0.  Labels of a vertex live on the rank that last
+ * propagated it (dlp_read_owned); reports are the global ones. */
+typedef int (*dlp_allreduce_fn)(void* ctx, int64_t* imax, int32_t nimax, int64_t* isum, int32_t nisum, double* dmax,
+                                int32_t ndmax);
+int dlp_shard_set(dlp_engine* e, int rank, int world);
+int dlp_apply_batch_sharded(dlp_engine* e, const dlp_config* cfg, const dlp_batch* batch, dlp_allreduce_fn reduce,
+                            void* ctx, dlp_report* reports);
+int dlp_read_owned(dlp_engine* e, uint8_t* owned, int64_t n);
+
 /* DynamicGraph.num_slots / num_alive (graph.py:189-192, 182). */
 int dlp_num_slots(dlp_engine* e, int64_t* n_slots, int64_t* num_alive);
 /* LabelState.f / .gt (labels.py:21-22).  f is [columns][n] row-major; GT

@@ -57,6 +57,9 @@ SIGNATURES = {
     "dlp_apply_structure": (_int, [_p, _p]),
     "dlp_itlp_batch": (_int, [_p, _p, _p, _p]),
     "dlp_reserve": (_int, [_p, _i64, _i64]),
+    "dlp_shard_set": (_int, [_p, _int, _int]),
+    "dlp_apply_batch_sharded": (_int, [_p, _p, _p, _p, _p, _p]),
+    "dlp_read_owned": (_int, [_p, _p, _i64]),
     "dlp_num_slots": (_int, [_p, _p, _p]),
     "dlp_read_labels": (_int, [_p, _p, _p, _i64]),
     "dlp_write_labels": (_int, [_p, _p, _i64]),

@@ -184,8 +184,142 @@ BatchDev stage_batch(Engine& E, const HostBatch& b) {
 
 enum Kind { KIND_DYNLP = 0, KIND_STRUCTURE = 1, KIND_ITLP = 2 };
 
+// Per-column engine.py:375-405 state machine for component-sharded batches,
+// driven by phase results reduced over all shards (the caller's collective).
+struct ColCtl {
+    long long iterations = 0, updates = 0, edges = 0, warnings = 0, certs = 0;
+    double max_change = 0.0;
+    int converged = 1, done = 0, has_fr = 0;
+    int act = ACT_NONE;
+};
+
+int sharded_lp(Engine& E, const dlp_config* cfg, long long max_iter, dlp_allreduce_fn reduce, void* rctx,
+               std::vector<ColCtl>& col, double* lp_ms, long long* launches) {
+    const int C = E.ncol;
+    // global F0 emptiness and eligible counts (replicated structure, sharded sets)
+    // label migration for components that changed owner (replicated order)
+    {
+        long long m = migr_collect(E, E.n_slots);
+        std::vector<int64_t> mi(1, m), ms(1, 0);
+        std::vector<double> md(1, 0.0);
+        if (reduce(rctx, mi.data(), 1, ms.data(), 1, md.data(), 1)) return fail(E, DLP_EINTERNAL, "collective failed");
+        if (mi[0] != m) return fail(E, DLP_EINTERNAL, "shards disagree on migrated vertices");
+        if (m) {
+            const size_t cnt = (size_t)m * C;
+            E.migr_buf.reserve(cnt, 0, E.st);
+            std::vector<double> hb(cnt);
+            migr_pack(E, m, E.migr_buf.p);
+            DLP_CUDA_TRY(cudaMemcpyAsync(hb.data(), E.migr_buf.p, cnt * 8, cudaMemcpyDeviceToHost, E.st));
+            DLP_CUDA_TRY(cudaStreamSynchronize(E.st));
+            std::vector<int64_t> z1(1, 0), z2(1, 0);
+            if (reduce(rctx, z1.data(), 1, z2.data(), 1, hb.data(), (int32_t)cnt))
+                return fail(E, DLP_EINTERNAL, "collective failed");
+            DLP_CUDA_TRY(cudaMemcpyAsync(E.migr_buf.p, hb.data(), cnt * 8, cudaMemcpyHostToDevice, E.st));
+            migr_unpack(E, m, E.migr_buf.p);
+            DLP_CUDA_TRY(cudaStreamSynchronize(E.st));
+        }
+    }
+    std::vector<int64_t> isum(2), imax(1, 0);
+    std::vector<double> dmax(1, 0.0);
+    DLP_CUDA_TRY(cudaMemcpyAsync(E.h_ds.p, E.ds, sizeof(DevState), cudaMemcpyDeviceToHost, E.st));
+    DLP_CUDA_TRY(cudaStreamSynchronize(E.st));
+    isum[0] = E.h_ds.p->n_f0;
+    isum[1] = E.h_ds.p->n_elist;
+    if (reduce(rctx, imax.data(), 1, isum.data(), 2, dmax.data(), 1)) return fail(E, DLP_EINTERNAL, "collective failed");
+    std::vector<long long> elig_g(C, isum[1]);
+    for (auto& c : col) c.has_fr = isum[0] > 0;
+    bool first = true;
+    auto t0 = std::chrono::steady_clock::now();
+    for (int launch = 0;; launch++) {
+        // decide each column's next action (mirrors decide_actions in lp.cu)
+        bool any = false;
+        for (int c = 0; c < C; c++) {
+            ColCtl& k = col[c];
+            k.act = ACT_NONE;
+            if (k.done) continue;
+            if (k.has_fr && k.iterations < max_iter) {
+                k.act = ACT_FRONTIER;
+            } else {
+                if (k.has_fr || k.iterations >= max_iter) {
+                    k.converged = k.has_fr ? 0 : 1;
+                    if (!k.converged) {
+                        k.done = 1;
+                        continue;
+                    }
+                }
+                if (elig_g[c] == 0) {  // certify swept nothing: break
+                    k.done = 1;
+                    continue;
+                }
+                k.act = ACT_CERTIFY;
+            }
+            any = true;
+        }
+        if (!any) break;
+        int act[kMaxCols] = {0};
+        long long budget[kMaxCols] = {0};
+        for (int c = 0; c < C; c++) {
+            act[c] = col[c].act;
+            budget[c] = max_iter - col[c].iterations;
+        }
+        DLP_CUDA_TRY(cudaMemcpyAsync(E.ctl->act, act, sizeof(act), cudaMemcpyHostToDevice, E.st));
+        DLP_CUDA_TRY(cudaMemcpyAsync(E.ctl->budget, budget, sizeof(budget), cudaMemcpyHostToDevice, E.st));
+        lp_run_actions(E, cfg->delta, first, false);
+        first = false;
+        DLP_CUDA_TRY(cudaMemcpyAsync(E.h_ctl.p, E.ctl, sizeof(LPCtl), cudaMemcpyDeviceToHost, E.st));
+        DLP_CUDA_TRY(cudaStreamSynchronize(E.st));
+        const LPCtl& L = *E.h_ctl.p;
+        // reduce: max rounds | sum updates, edges, warnings, frontier, eligible | max rmax
+        std::vector<int64_t> rmaxv(C), sums(5 * C);
+        std::vector<double> dm(C);
+        for (int c = 0; c < C; c++) {
+            rmaxv[c] = L.ph_rounds[c];
+            sums[c] = L.ph_upd[c];
+            sums[C + c] = L.ph_edges[c];
+            sums[2 * C + c] = L.ph_warn[c];
+            sums[3 * C + c] = L.has_fr[c];
+            sums[4 * C + c] = L.elig_count[c];
+            dm[c] = col[c].act == ACT_CERTIFY ? L.ph_mc[c] : 0.0;
+        }
+        if (reduce(rctx, rmaxv.data(), C, sums.data(), 5 * C, dm.data(), C))
+            return fail(E, DLP_EINTERNAL, "collective failed");
+        // the frontier phase's max_change is its last global round's: shards that
+        // ran fewer rounds had an empty frontier in that round
+        std::vector<int64_t> none(1, 0), nsum(1, 0);
+        std::vector<double> mc(C, -1.0);
+        for (int c = 0; c < C; c++)
+            if (col[c].act == ACT_FRONTIER && L.ph_rounds[c] == rmaxv[c] && rmaxv[c] > 0) mc[c] = L.ph_mc[c];
+        if (reduce(rctx, none.data(), 1, nsum.data(), 1, mc.data(), C)) return fail(E, DLP_EINTERNAL, "collective failed");
+        for (int c = 0; c < C; c++) {
+            ColCtl& k = col[c];
+            elig_g[c] = sums[4 * C + c];
+            if (k.act == ACT_NONE) continue;
+            k.updates += sums[c];
+            k.edges += sums[C + c];
+            k.warnings += sums[2 * C + c];
+            k.has_fr = sums[3 * C + c] > 0;
+            if (k.act == ACT_FRONTIER) {
+                k.iterations += rmaxv[c];
+                if (rmaxv[c] > 0) k.max_change = mc[c];
+            } else {  // certify_round committed (engine.py:398-405)
+                k.iterations += 1;
+                k.certs += 1;
+                k.max_change = dm[c];
+                if (dm[c] <= cfg->delta) k.done = 1;
+            }
+        }
+    }
+    if (!first) {  // clear leftover frontier masks for the next batch
+        lp_run_actions(E, cfg->delta, false, true);
+        DLP_CUDA_TRY(cudaStreamSynchronize(E.st));
+    }
+    *lp_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    (void)launches;
+    return DLP_OK;
+}
+
 int run_batch(dlp_engine* h, const dlp_config* cfg, const dlp_batch* batch, bool device_ptrs, bool trusted,
-              dlp_report* reps, Kind kind) {
+              dlp_report* reps, Kind kind, dlp_allreduce_fn reduce = nullptr, void* rctx = nullptr) {
     Engine& E = h->E;
     auto t0 = std::chrono::steady_clock::now();
     if (h->poisoned) return fail(E, DLP_EINTERNAL, "engine is unusable after an earlier CUDA error");
@@ -310,6 +444,36 @@ int run_batch(dlp_engine* h, const dlp_config* cfg, const dlp_batch* batch, bool
                 init_components_dev(E, bd, base);
             }
             reach_and_pin_dev(E, full_cc, n);
+            if (reduce) {  // component-sharded propagation
+                std::vector<ColCtl> col(E.ncol);
+                double ms = 0.0;
+                int rc = sharded_lp(E, cfg, max_iter, reduce, rctx, col, &ms, nullptr);
+                if (rc) return rc;
+                DLP_CUDA_TRY(cudaMemcpyAsync(E.h_ds.p, E.ds, sizeof(DevState), cudaMemcpyDeviceToHost, E.st));
+                DLP_CUDA_TRY(cudaStreamSynchronize(E.st));
+                DevState& s = *E.h_ds.p;
+                E.live_edges = s.log_n;
+                E.pool_top_host = (long long)s.pool_top;
+                E.last_tau = s.tau;
+                E.cc_valid = true;
+                for (int c = 0; c < E.ncol; c++) {
+                    dlp_report& r = reps[c];
+                    r.iterations = col[c].iterations;
+                    r.updates = col[c].updates;
+                    r.max_change = col[c].max_change;
+                    r.converged = col[c].converged;
+                    r.isolated_pinned = s.isolated;
+                    r.unreachable_pinned = s.unreach;
+                    r.warnings = col[c].warnings + r.isolated_pinned + r.unreachable_pinned;
+                    r.edges_traversed = col[c].edges;
+                    r.certify_sweeps = col[c].certs;
+                    r.lp_kernel_ms = ms;
+                    r.gpu_launches = E.launches - launches0;
+                    r.lp_rounds = col[c].iterations;
+                }
+                finish_time();
+                return DLP_OK;
+            }
             lp_run_dev(E, cfg->delta, max_iter, false);
         } else {  // ItLP: no reachability, active = alive & unlabeled & deg > 0
             itlp_active_dev(E, n);
@@ -414,6 +578,37 @@ int dlp_create(const dlp_config* cfg, int device, dlp_engine** out) {
     return DLP_OK;
 }
 
+int dlp_shard_set(dlp_engine* h, int rank, int world) {
+    if (!h) return DLP_EINTERNAL;
+    Engine& E = h->E;
+    if (world < 1 || world > 255 || rank < 0 || rank >= world) return fail(E, DLP_EVALIDATION, "bad shard rank/world");
+    E.shard_rank = rank;
+    E.shard_world = world;
+    return DLP_OK;
+}
+
+int dlp_apply_batch_sharded(dlp_engine* h, const dlp_config* cfg, const dlp_batch* batch, dlp_allreduce_fn reduce,
+                            void* ctx, dlp_report* reports) {
+    if (!h) return DLP_EINTERNAL;
+    if (!reduce) return fail(h->E, DLP_EVALIDATION, "a reduction callback is required");
+    return run_batch(h, cfg, batch, false, false, reports, KIND_DYNLP, reduce, ctx);
+}
+
+int dlp_read_owned(dlp_engine* h, uint8_t* owned, int64_t n) {
+    if (!h) return DLP_EINTERNAL;
+    Engine& E = h->E;
+    if (n != E.n_slots) return fail(E, DLP_EVALIDATION, "n must equal num_slots");
+    try {
+        DLP_CUDA_TRY(cudaSetDevice(E.device));
+        std::vector<unsigned char> o(n);
+        if (n) DLP_CUDA_TRY(cudaMemcpy(o.data(), E.owner_rank.p, n, cudaMemcpyDeviceToHost));
+        for (long long v = 0; v < n; v++) owned[v] = E.shard_world <= 1 || o[v] == E.shard_rank;
+    } catch (const CudaFailure& f) {
+        return cuda_fail(h, f);
+    }
+    return DLP_OK;
+}
+
 int dlp_reserve(dlp_engine* h, int64_t n_vertices, int64_t n_edges) {
     if (!h) return DLP_EINTERNAL;
     Engine& E = h->E;
@@ -437,7 +632,12 @@ int dlp_destroy(dlp_engine* h) {
     Engine& E = h->E;
     cudaSetDevice(E.device);
     cudaStreamSynchronize(E.st);
-    DevArray<unsigned char>* u8s[] = {&E.alive, &E.mark, &E.root_gt, &E.d_stage, &E.cub_tmp};
+    DevArray<unsigned char>* u8s[] = {&E.alive, &E.mark, &E.root_gt, &E.owner_rank, &E.migr_from, &E.d_stage,
+                                      &E.cub_tmp};
+    E.migr_flag.release();
+    E.migr_pos.release();
+    E.migr_list.release();
+    E.migr_buf.release();
     for (auto* a : u8s) a->release();
     E.purge_flag.release();
     E.gt.release();

@@ -86,7 +86,22 @@ struct LPCtl {
     long long trace_cap;
     int* seen;               // debug: per-vertex round stamp (duplicate work items)
     unsigned long long dups; // debug: duplicate work items detected
+    // ---- action mode (component-sharded execution): the host
+    // runs each column's engine.py:375-405 state machine on phase results
+    // reduced over all shards; a launch executes one action per column.
+    int act[kMaxCols];             // ACT_NONE / ACT_FRONTIER / ACT_CERTIFY
+    long long budget[kMaxCols];    // round budget of a frontier phase
+    int has_fr[kMaxCols];          // column has a (local) frontier in the lists
+    long long ph_rounds[kMaxCols]; // rounds executed by the action
+    long long ph_upd[kMaxCols];
+    long long ph_edges[kMaxCols];
+    long long ph_warn[kMaxCols];
+    double ph_mc[kMaxCols];        // max |delta| of the action's last round
+    long long r_par;               // rounds executed in this batch (list parity)
+    unsigned int ncur_p[3];        // frontier list lengths at exit
+    int started;                   // prologue done for this batch
 };
+enum { ACT_NONE = 0, ACT_FRONTIER = 1, ACT_CERTIFY = 2 };
 
 template <typename T>
 struct DevArray {
@@ -157,9 +172,12 @@ struct Engine {
     double last_tau = 0.0;
     long long intra_k = 0;
     bool cc_valid = true;  // global union-find consistent with the live graph
+    int shard_rank = 0, shard_world = 1;  // component sharding (dlp_shard_set)
 
     // per-vertex ----------------------------------------------------------
-    DevArray<unsigned char> alive, mark, root_gt;
+    DevArray<unsigned char> alive, mark, root_gt, owner_rank, migr_from;
+    DevArray<int> migr_flag, migr_pos, migr_list;
+    DevArray<double> migr_buf;
     DevArray<int> purge_flag;
     DevArray<signed char> gt;
     DevArray<long long> row_start;
@@ -215,9 +233,13 @@ void intra_components_dev(Engine& E, const BatchDev& b, long long base);
 void init_components_dev(Engine& E, const BatchDev& b, long long base);
 void reach_and_pin_dev(Engine& E, bool full_rebuild, long long n);
 void compact_pool(Engine& E, long long min_free);
+long long migr_collect(Engine& E, long long n);
+void migr_pack(Engine& E, long long m, double* dev_buf);
+void migr_unpack(Engine& E, long long m, const double* dev_buf);
 void host_mark(Engine& E, const char* what);
 // lp.cu ---------------------------------------------------------------------
 void lp_run_dev(Engine& E, double delta, long long max_iter, bool itlp);
+void lp_run_actions(Engine& E, double delta, bool first, bool cleanup);
 void lp_setup(Engine& E);
 void lp_dump_trace(Engine& E, long long rounds);
 void itlp_active_dev(Engine& E, long long n);

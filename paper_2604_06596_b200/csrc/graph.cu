@@ -48,6 +48,11 @@ void ensure_vertex_capacity(Engine& E, long long want) {
     grow_zero(E.alive, nc, keep, st);
     grow_zero(E.mark, nc, keep, st);
     grow_zero(E.root_gt, nc, keep, st);
+    grow_zero(E.owner_rank, nc, keep, st);
+    grow_zero(E.migr_from, nc, keep, st);
+    E.migr_flag.reserve(nc + 1, 0, st);
+    E.migr_pos.reserve(nc + 1, 0, st);
+    E.migr_list.reserve(nc + 1, 0, st);
     grow_zero(E.gt, nc, keep, st);
     grow_zero(E.row_start, nc, keep, st);
     grow_zero(E.row_len, nc, keep, st);
@@ -963,15 +968,39 @@ __global__ void k_uf_flatten_root_gt(int* par, long long n, const unsigned char*
 }
 
 
+// component owner under sharding: a mixing hash of the
+// component's canonical root (minimum member id), identical on every rank
+__device__ inline int shard_owner(int root, int world) {
+    unsigned int h = (unsigned int)root * 2654435761u;
+    h ^= h >> 16;
+    return (int)(h % (unsigned int)world);
+}
+
 __global__ void k_eligible(long long n, int ncol, long long cap, const unsigned char* alive, const signed char* gt,
                            const int* par, const unsigned char* root_gt, const int* row_len, unsigned char* mark,
-                           unsigned int* eligm, double* f0, double* f1, int* elist, int* f0list, DevState* ds) {
+                           unsigned int* eligm, double* f0, double* f1, int* elist, int* f0list, DevState* ds,
+                           int rank, int world, unsigned char* owner_rank, unsigned char* migr_from,
+                           int* migr_flag) {
     unsigned int allc = ncol >= 32 ? 0xffffffffu : ((1u << ncol) - 1u);
     long long iso = 0, unr = 0;
     for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < n; v += (long long)gridDim.x * blockDim.x) {
         bool unl = alive[v] && gt[v] == -1;
         bool reached = alive[v] && root_gt[par[v]];
         bool e = unl && reached;
+        if (world > 1) {  // sharded: only this rank's components are propagated here
+            int mig = 0;
+            if (e) {
+                int o = shard_owner(par[v], world);
+                int prev = owner_rank[v];
+                if (o != prev) {  // component moved: its label lives on rank `prev`
+                    mig = 1;
+                    migr_from[v] = (unsigned char)prev;
+                    owner_rank[v] = (unsigned char)o;
+                }
+                e = o == rank;
+            }
+            migr_flag[v] = mig;
+        }
         eligm[v] = e ? allc : 0u;
         if (unl && !reached) {
             for (int c = 0; c < ncol; c++) {
@@ -1019,7 +1048,60 @@ void reach_and_pin_dev(Engine& E, bool full_rebuild, long long n) {
     E.launches++;
     k_eligible<<<grid_for(n), kBlock, 0, st>>>(n, E.ncol, E.cap_n, E.alive.p, E.gt.p, E.parent.p, E.root_gt.p,
                                                E.row_len.p, E.mark.p, E.eligm.p, E.f[0].p, E.f[1].p, E.elist.p, E.f0.p,
-                                               E.ds);
+                                               E.ds, E.shard_rank, E.shard_world, E.owner_rank.p, E.migr_from.p,
+                                               E.migr_flag.p);
+    E.launches++;
+}
+
+// ---------------------------------------------------------------------------
+// sharded label migration: vertices whose component changed owner get their
+// label from the previous owner (exchanged with the caller's max-reduction;
+// non-owners contribute -inf, so the result is bit-exact)
+// ---------------------------------------------------------------------------
+__global__ void k_migr_list(const int* flag, const int* pos, long long n, int* list) {
+    for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < n; v += (long long)gridDim.x * blockDim.x)
+        if (flag[v]) list[pos[v]] = (int)v;
+}
+__global__ void k_migr_pack(const int* list, long long m, int ncol, int rank, const unsigned char* from,
+                            const double* X, double* buf) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m * ncol;
+         i += (long long)gridDim.x * blockDim.x) {
+        int v = list[i / ncol], c = (int)(i % ncol);
+        buf[i] = from[v] == rank ? X[(long long)v * ncol + c] : -INFINITY;
+    }
+}
+__global__ void k_migr_unpack(const int* list, long long m, int ncol, const double* buf, double* X) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m * ncol;
+         i += (long long)gridDim.x * blockDim.x) {
+        int v = list[i / ncol], c = (int)(i % ncol);
+        X[(long long)v * ncol + c] = buf[i];
+    }
+}
+
+long long migr_collect(Engine& E, long long n) {
+    cudaStream_t st = E.st;
+    if (n == 0) return 0;
+    cub_scan(E, E.migr_flag.p, E.migr_pos.p, n);
+    int lp = 0, lf = 0;
+    DLP_CUDA_TRY(cudaMemcpyAsync(&lp, E.migr_pos.p + n - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+    DLP_CUDA_TRY(cudaMemcpyAsync(&lf, E.migr_flag.p + n - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+    DLP_CUDA_TRY(cudaStreamSynchronize(st));
+    long long m = (long long)lp + lf;
+    if (m) {
+        k_migr_list<<<grid_for(n), kBlock, 0, st>>>(E.migr_flag.p, E.migr_pos.p, n, E.migr_list.p);
+        E.launches++;
+    }
+    return m;
+}
+
+void migr_pack(Engine& E, long long m, double* dev_buf) {
+    k_migr_pack<<<grid_for(m * E.ncol), kBlock, 0, E.st>>>(E.migr_list.p, m, E.ncol, E.shard_rank, E.migr_from.p,
+                                                           E.f[0].p, dev_buf);
+    E.launches++;
+}
+
+void migr_unpack(Engine& E, long long m, const double* dev_buf) {
+    k_migr_unpack<<<grid_for(m * E.ncol), kBlock, 0, E.st>>>(E.migr_list.p, m, E.ncol, dev_buf, E.f[0].p);
     E.launches++;
 }
 

@@ -40,6 +40,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstddef>
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -102,6 +103,8 @@ struct LPParams {
     long long n;  // vertex slots
     int C;
     int itlp;
+    int action_mode;  // execute ctl->act[] once per column, then exit (sharded batches)
+    int cleanup;      // action mode: clear the leftover frontier masks and exit
 };
 
 struct ColState {
@@ -264,6 +267,49 @@ __device__ void decide_actions(ColState& S, const LPParams& P, const unsigned lo
         }
         ce |= bit;
         done = 0;
+    }
+    S.fr_mask = fr;
+    S.cert_mask = ce;
+    S.done = done;
+}
+
+// Action-mode controller: columns execute the action the host assigned and
+// stop at its end (frontier phase: local frontier empty or budget reached;
+// certify: one round).  Phase statistics accumulate in S and go to ctl.
+__device__ void decide_actions_act(ColState& S, const LPParams& P, const unsigned long long* res,
+                                   const unsigned int* claimed, int first) {
+    const int C = P.C;
+    unsigned int fr = 0, ce = 0;
+    int done = 1;
+    for (int c = 0; c < C; c++) {
+        const unsigned int bit = 1u << c;
+        if (S.phase[c] == PH_DONE) continue;
+        const int act = P.ctl->act[c];
+        if (!first) {
+            const bool was_fr = (S.fr_mask & bit) != 0, was_ce = (S.cert_mask & bit) != 0;
+            if (was_fr || was_ce) {
+                S.iterations[c]++;  // rounds of this action
+                S.updates[c] += (long long)res[kMaxCols + c];
+                S.edges[c] += (long long)res[2 * kMaxCols + c];
+                S.warnings[c] += (long long)res[3 * kMaxCols + c];
+                S.max_change[c] = __longlong_as_double((long long)res[c]);
+                S.has_frontier[c] = (*claimed & bit) != 0;
+                if (was_ce) {
+                    S.phase[c] = PH_DONE;
+                    continue;
+                }
+            }
+        }
+        if (act == ACT_FRONTIER && S.has_frontier[c] && S.iterations[c] < P.ctl->budget[c]) {
+            fr |= bit;
+            done = 0;
+        } else if (act == ACT_CERTIFY && S.it_run[c] == 0) {
+            S.it_run[c] = 1;
+            ce |= bit;
+            done = 0;
+        } else {
+            S.phase[c] = PH_DONE;
+        }
     }
     S.fr_mask = fr;
     S.cert_mask = ce;
@@ -569,55 +615,65 @@ __global__ void __launch_bounds__(kLpThreads, DLP_LP_MINB) k_lp_fused(LPParams P
     const long long n = P.n;
 
     // ---- prologue: F0 (engine.py:364-367) is every column's first frontier;
-    // the eligible list and F0 are split by row class
+    // the eligible list and F0 are split by row class.  In action mode only
+    // the first launch of a batch runs it; later launches resume the lists.
+    const bool resume = P.action_mode && ctl->started;
     const long long n0 = P.itlp ? 0 : P.ds->n_f0;
     const long long n_el = P.ds->n_elist;
-    for (long long i = gtid; i < n0; i += gth) {
-        int u = P.f0[i];
-        P.fmask[0][u] = allc;
-        // one call site per class: append_u32 aggregates over the converged
-        // threads, which must all target the same list
-        switch (row_class(P.row_len[u])) {
-            case CLS_SHORT: append_u32(P.flist[0][0], &ctl->n_f0[0], u); break;
-            case CLS_LONG: append_u32(P.flist[1][0], &ctl->n_f0[1], u); break;
-            default: append_u32(P.flist[2][0], &ctl->n_f0[2], u); break;
+    if (!resume) {
+        for (long long i = gtid; i < n0; i += gth) {
+            int u = P.f0[i];
+            P.fmask[0][u] = allc;
+            // one call site per class: append_u32 aggregates over the converged
+            // threads, which must all target the same list
+            switch (row_class(P.row_len[u])) {
+                case CLS_SHORT: append_u32(P.flist[0][0], &ctl->n_f0[0], u); break;
+                case CLS_LONG: append_u32(P.flist[1][0], &ctl->n_f0[1], u); break;
+                default: append_u32(P.flist[2][0], &ctl->n_f0[2], u); break;
+            }
         }
-    }
-    for (long long i = gtid; i < n_el; i += gth) {
-        int u = P.elist[i];
-        const int cls = row_class(P.row_len[u]);
-        P.eligm[u] |= (unsigned int)cls << kClassShift;
-        switch (cls) {
-            case CLS_SHORT: append_u32(P.elist_c[0], &ctl->n_el[0], u); break;
-            case CLS_LONG: append_u32(P.elist_c[1], &ctl->n_el[1], u); break;
-            default: append_u32(P.elist_c[2], &ctl->n_el[2], u); break;
+        for (long long i = gtid; i < n_el; i += gth) {
+            int u = P.elist[i];
+            const int cls = row_class(P.row_len[u]);
+            P.eligm[u] |= (unsigned int)cls << kClassShift;
+            switch (cls) {
+                case CLS_SHORT: append_u32(P.elist_c[0], &ctl->n_el[0], u); break;
+                case CLS_LONG: append_u32(P.elist_c[1], &ctl->n_el[1], u); break;
+                default: append_u32(P.elist_c[2], &ctl->n_el[2], u); break;
+            }
         }
     }
     if (tid == 0) {
         for (int c = 0; c < C; c++) {
             S.phase[c] = PH_FRONTIER;
-            S.has_frontier[c] = n0 > 0;
+            S.has_frontier[c] = resume ? ctl->has_fr[c] : (n0 > 0);
             S.it_run[c] = 0;
             S.mc_last[c] = 0.0;
             S.iterations[c] = S.updates[c] = S.certs[c] = S.warnings[c] = S.edges[c] = 0;
             S.max_change[c] = 0.0;
             S.converged[c] = P.itlp ? (n_el == 0) : 1;
             if (P.itlp && n_el == 0) S.phase[c] = PH_DONE;
+            if (P.action_mode && (P.cleanup || ctl->act[c] == ACT_NONE)) S.phase[c] = PH_DONE;
         }
         S.fr_mask = S.cert_mask = 0;
-        if (blockIdx.x == 0)
+        if (blockIdx.x == 0 && !resume)
             for (int c = 0; c < C; c++) ctl->elig_count[c] = n_el;
     }
     grid_sync(&ctl->bar, target);
-    if (tid == 0) decide_actions(S, P, nullptr, nullptr, 1);
+    if (tid == 0) {
+        if (P.action_mode)
+            decide_actions_act(S, P, nullptr, nullptr, 1);
+        else
+            decide_actions(S, P, nullptr, nullptr, 1);
+    }
     long long nel[3], ncur[3];
     for (int j = 0; j < 3; j++) {
         nel[j] = *(volatile unsigned int*)&ctl->n_el[j];
-        ncur[j] = *(volatile unsigned int*)&ctl->n_f0[j];
+        ncur[j] = resume ? *(volatile unsigned int*)&ctl->ncur_p[j] : *(volatile unsigned int*)&ctl->n_f0[j];
     }
     __syncthreads();
 
-    long long R = 0;
+    long long R = resume ? ctl->r_par : 0;
     while (!S.done) {
         const unsigned int FR = S.fr_mask, CE = S.cert_mask;
         const int ri = (int)(R & 1), rn = ri ^ 1;
@@ -786,7 +842,12 @@ __global__ void __launch_bounds__(kLpThreads, DLP_LP_MINB) k_lp_fused(LPParams P
                 ctl->uentries += (long long)vs->uentries;
             }
             __syncthreads();
-            if (tid == 0) decide_actions(S, P, s_res, &s_claimed, 0);
+            if (tid == 0) {
+                if (P.action_mode)
+                    decide_actions_act(S, P, s_res, &s_claimed, 0);
+                else
+                    decide_actions(S, P, s_res, &s_claimed, 0);
+            }
         }
         for (int j = 0; j < 3; j++) ncur[j] = s_cnt[j];
         if (ctl->trace && gtid == 0 && R < ctl->trace_cap) {
@@ -801,6 +862,25 @@ __global__ void __launch_bounds__(kLpThreads, DLP_LP_MINB) k_lp_fused(LPParams P
         R++;
         __syncthreads();
     }
+    if (P.action_mode && !P.cleanup) {
+        // hand the lists and per-column phase results to the host
+        grid_sync(&ctl->bar, target);  // every CTA has read ctl before it is rewritten
+        if (gtid == 0) {
+            for (int c = 0; c < C; c++) {
+                ctl->has_fr[c] = S.has_frontier[c];
+                ctl->ph_rounds[c] = S.iterations[c];
+                ctl->ph_upd[c] = S.updates[c];
+                ctl->ph_edges[c] = S.edges[c];
+                ctl->ph_warn[c] = S.warnings[c];
+                ctl->ph_mc[c] = S.max_change[c];
+            }
+            for (int j = 0; j < 3; j++) ctl->ncur_p[j] = (unsigned int)ncur[j];
+            ctl->r_par = R;
+            ctl->started = 1;
+            ctl->rounds = R;
+        }
+        return;
+    }
     // leftover frontiers (budget exhausted): clear their masks for the next batch
     {
         const int ri = (int)(R & 1);
@@ -811,7 +891,7 @@ __global__ void __launch_bounds__(kLpThreads, DLP_LP_MINB) k_lp_fused(LPParams P
             P.fmask[ri][u] = 0;
         }
     }
-    if (gtid == 0) {
+    if (gtid == 0 && !P.action_mode) {
         for (int c = 0; c < C; c++) {
             ctl->iterations[c] = S.iterations[c];
             ctl->updates[c] = S.updates[c];
@@ -878,6 +958,8 @@ void lp_run_dev(Engine& E, double delta, long long max_iter, bool itlp) {
     P.n = E.n_slots;
     P.C = E.ncol;
     P.itlp = itlp ? 1 : 0;
+    P.action_mode = 0;
+    P.cleanup = 0;
     DLP_CUDA_TRY(cudaMemsetAsync(E.ctl, 0, sizeof(LPCtl), E.st));
     if (E.lp_trace_path) {
         const long long cap = 1 << 16;
@@ -896,6 +978,52 @@ void lp_run_dev(Engine& E, double delta, long long max_iter, bool itlp) {
     DLP_CUDA_TRY(cudaLaunchCooperativeKernel((void*)k_lp_fused, dim3(E.lp_grid), dim3(kLpThreads), args, E.lp_smem,
                                              E.st));
     DLP_CUDA_TRY(cudaEventRecord(E.lp_ev[1], E.st));
+    E.launches++;
+}
+
+// One action-mode launch (component-sharded batches): the host has written
+// ctl->act / ctl->budget; first = first launch of the batch (full reset).
+void lp_run_actions(Engine& E, double delta, bool first, bool cleanup) {
+    lp_setup(E);
+    LPParams P;
+    P.row_start = E.row_start.p;
+    P.row_len = E.row_len.p;
+    P.nbr = E.nbr.p;
+    P.w = E.wgt.p;
+    P.X = E.f[0].p;
+    P.Y = E.f[1].p;
+    P.eligm = E.eligm.p;
+    P.emask_store = E.emask_store.p;
+    for (int i = 0; i < 2; i++) {
+        P.fmask[i] = E.fmask[i].p;
+        P.flist[0][i] = E.ulist[i].p;
+        P.flist[1][i] = E.llist[i].p;
+        P.flist[2][i] = E.hlist[i].p;
+    }
+    P.elist_c[0] = E.elist_s.p;
+    P.elist_c[1] = E.elist_l.p;
+    P.elist_c[2] = E.elist_h.p;
+    P.f0 = E.f0.p;
+    P.elist = E.elist.p;
+    P.ds = E.ds;
+    P.ctl = E.ctl;
+    P.delta = delta;
+    P.max_iter = 0;
+    P.n = E.n_slots;
+    P.C = E.ncol;
+    P.itlp = 0;
+    P.action_mode = 1;
+    P.cleanup = cleanup ? 1 : 0;
+    if (first) {
+        // keep the host-written actions across the reset
+        DLP_CUDA_TRY(cudaMemsetAsync(E.ctl, 0, offsetof(LPCtl, act), E.st));
+        DLP_CUDA_TRY(cudaMemsetAsync(&E.ctl->has_fr, 0, sizeof(LPCtl) - offsetof(LPCtl, has_fr), E.st));
+    } else {
+        DLP_CUDA_TRY(cudaMemsetAsync(&E.ctl->bar, 0, sizeof(unsigned int), E.st));
+    }
+    void* args[] = {&P};
+    DLP_CUDA_TRY(cudaLaunchCooperativeKernel((void*)k_lp_fused, dim3(E.lp_grid), dim3(kLpThreads), args, E.lp_smem,
+                                             E.st));
     E.launches++;
 }
 

@@ -1,0 +1,121 @@
+"""Component sharding.
+
+CPU (gloo, world_size 2): the torch collective the engine's phase reduction
+uses.  GPU: the sharded protocol as virtual shards on one device (threads +
+in-process reduction, same C++ state machine and action-mode kernel the
+NCCL path runs), bit-identical to the unsharded engine: reports and merged
+labels."""
+
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _gloo_worker(rank, world, port, q):
+    sys.path.insert(0, os.path.dirname(HERE))
+    import torch.distributed as dist
+
+    from paper_2604_06596_b200.sharded import torch_collective
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    coll = torch_collective()
+    imax = np.array([rank * 10, 5 - rank], dtype=np.int64)
+    isum = np.array([rank + 1, 100], dtype=np.int64)
+    dmax = np.array([0.25 * rank, -1.0 + rank], dtype=np.float64)
+    coll(imax, isum, dmax)
+    q.put((rank, imax.tolist(), isum.tolist(), dmax.tolist()))
+    dist.destroy_process_group()
+
+
+def test_torch_collective_gloo_world2():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_gloo_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    out = [q.get(timeout=120) for _ in ps]
+    for p in ps:
+        p.join(timeout=60)
+    for rank, imax, isum, dmax in out:
+        assert imax == [10, 5] and isum == [3, 200] and dmax == [0.25, 0.0]
+
+
+def test_in_process_collective_threads():
+    import threading
+
+    from paper_2604_06596_b200.sharded import InProcessCollective
+
+    coll = InProcessCollective(3)
+    res = {}
+
+    def w(r):
+        a, b, d = np.array([r]), np.array([r, 1]), np.array([float(-r)])
+        coll.for_rank(r)(a, b, d)
+        res[r] = (a.tolist(), b.tolist(), d.tolist())
+
+    th = [threading.Thread(target=w, args=(r,)) for r in range(3)]
+    [t.start() for t in th]
+    [t.join() for t in th]
+    assert all(v == ([2], [3, 3], [0.0]) for v in res.values())
+
+
+def _unsharded(batches, cfg, ncls):
+    from paper_2604_06596_b200.engine import DynamicGraph, LabelState, apply_batch
+
+    g, lab = DynamicGraph(0, num_classes=ncls), LabelState()
+    out = []
+    for b in batches:
+        lab, rep = apply_batch(g, lab, b, cfg)
+        out.append((rep if isinstance(rep, list) else [rep], lab.F.copy()))
+    g.close()
+    return out
+
+
+def _stream(kind):
+    from paper_2604_06596_b200 import streams
+
+    if kind == "blobs10":  # well-separated blobs: many components to distribute
+        bl = streams.make_blobs(5000, 16, 10, 3, spread=40.0)
+        e = streams.knn_graph_exact(bl.x, 8)
+        gt = streams.stratified_seeds(bl.classes, 0.02, 3)
+        return streams.phased_stream(5000, e, bl.classes, gt, 500, 3, 0.75, 0.02, 0.23, initial_gt=20).batches, 10
+    bl = streams.make_blobs(4000, 8, 2, 4, spread=30.0)
+    e = streams.knn_graph_exact(bl.x, 6)
+    gt = streams.stratified_seeds(bl.classes, 0.02, 4)
+    return streams.phased_stream(4000, e, bl.classes, gt, 400, 4, 0.7, 0.02, 0.28, initial_gt=4).batches, 2
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind,world", [("blobs2", 2), ("blobs10", 2), ("blobs10", 3)])
+def test_virtual_shards_bit_identical(gpu_device, kind, world):
+    from paper_2604_06596_b200.engine import EngineConfig
+    from paper_2604_06596_b200.sharded import run_virtual_shards
+
+    batches, ncls = _stream(kind)
+    cfg = EngineConfig(delta=1e-5)
+    want = _unsharded(batches, cfg, ncls)
+    got = run_virtual_shards(batches, cfg, world, num_classes=ncls)
+    for t, ((rw, Fw), (rg, Fg)) in enumerate(zip(want, got)):
+        rg = rg if isinstance(rg, list) else [rg]
+        for c, (a, b) in enumerate(zip(rw, rg)):
+            ta = (a.iterations, a.updates, a.max_change, a.converged, a.warnings, a.edges_traversed,
+                  a.certify_sweeps)
+            tb = (b.iterations, b.updates, b.max_change, b.converged, b.warnings, b.edges_traversed,
+                  b.certify_sweeps)
+            assert ta == tb, f"batch {t} column {c}: {ta} != {tb}"
+        assert Fw.tobytes() == Fg.tobytes(), f"batch {t}: labels differ"
