@@ -618,7 +618,9 @@ int dlp_reserve(dlp_engine* h, int64_t n_vertices, int64_t n_edges) {
         DLP_CUDA_TRY(cudaSetDevice(E.device));
         ensure_vertex_capacity(E, n_vertices + 1);
         ensure_log(E, n_edges + 1);
-        long long want = 2 * n_edges + (2 * n_edges) / 2 + 4 * n_vertices;
+        // live entries with compaction slack (25%) + fresh-row space, plus the
+        // free headroom compact_pool keeps (a quarter of the pool): no growth later
+        long long want = ((2 * n_edges) * 5 / 4 + 4 * n_vertices + (1 << 20)) * 4 / 3 + (1 << 20);
         if (E.pool_cap < want) compact_pool(E, want - 2 * E.live_edges);
         DLP_CUDA_TRY(cudaStreamSynchronize(E.st));
     } catch (const CudaFailure& f) {

@@ -538,7 +538,7 @@ void apply_inserts_dev(Engine& E, const BatchDev& b, long long base) {
         long long need = (long long)E.h_ds.p->pool_need, top = (long long)E.h_ds.p->pool_top;
         if (top + need > E.pool_cap) {
             host_mark(E, "pre-compact");
-            compact_pool(E, std::max<long long>(16 * need, E.pool_cap / 4));
+            compact_pool(E, std::max<long long>(16 * need, E.pool_cap / 8));
             host_mark(E, "compact");
         }
     }

@@ -355,25 +355,40 @@ struct RoundCtx {
 // entry-parallel gathers staged in warp-private shared memory (product terms
 // precomputed), then lane (row, column) runs the ordered sums; finally the
 // changed rows claim themselves and their neighbours.
+// Row metadata of one tile row (lane r holds row r): loads issued one tile
+// ahead so their latency hides behind the current tile's gathers.
+struct TileMeta {
+    int u, len;
+    unsigned int em;
+    long long st;
+};
+__device__ inline TileMeta load_meta(const LPParams& P, const RoundCtx& R, int u) {
+    TileMeta m{u, 0, 0u, 0};
+    if (u >= 0) {
+        m.em = P.itlp ? (R.CE & P.eligm[u]) : (((R.fm_cur[u] & R.FR) | R.CE) & P.eligm[u]);
+        m.st = P.row_start[u];
+        m.len = P.row_len[u];
+    }
+    return m;
+}
+
+// Evaluate the tile (rows W[k0 ..], metadata m); `un` is the next tile's row
+// of this lane (-1 if none), whose metadata is loaded into *mn mid-tile.
 __device__ void warp_tile(const LPParams& P, const RoundCtx& R, ClaimCtx& K, BlockCounters& B, WarpTile& T,
-                          double* sw, double* sx, double* sfu, long long k0, int nrows, unsigned long long pol) {
+                          double* sw, double* sx, double* sfu, long long k0, int nrows, unsigned long long pol,
+                          const TileMeta& m, int un, TileMeta* mn) {
     const int C = P.C;
     const int lane = threadIdx.x & 31;
     // ---- tile rows
     int len = 0;
     unsigned int em = 0;
     if (lane < nrows) {
-        int u = R.W[k0 + lane];
-        em = P.itlp ? (R.CE & P.eligm[u]) : (((R.fm_cur[u] & R.FR) | R.CE) & P.eligm[u]);
-        P.emask_store[u] = em;
-        long long st = 0;
-        if (em) {
-            st = P.row_start[u];
-            len = P.row_len[u];
-        }
-        T.u[lane] = u;
+        em = m.em;
+        P.emask_store[m.u] = em;
+        len = em ? m.len : 0;
+        T.u[lane] = m.u;
         T.em[lane] = em;
-        T.st[lane] = st;
+        T.st[lane] = em ? m.st : 0;
         T.len[lane] = len;
     }
     __syncwarp();  // T.* written by lane r is read by other lanes below
@@ -396,6 +411,7 @@ __device__ void warp_tile(const LPParams& P, const RoundCtx& R, ClaimCtx& K, Blo
         int r = i / C, c = i - r * C;
         sfu[i] = ((T.em[r] >> c) & 1u) ? P.X[(long long)T.u[r] * C + c] : 0.0;
     }
+    *mn = load_meta(P, R, un);  // next tile's metadata, consumed next iteration
     __syncwarp();
     // ---- accumulate lanes
     const int ar = lane / C, ac = lane - ar * C;
@@ -483,6 +499,35 @@ __device__ void warp_tile(const LPParams& P, const RoundCtx& R, ClaimCtx& K, Blo
             atomicOr(&K.fm_next[v], m);  // no return value: a fire-and-forget RED
         else
             claim(K, v, m);
+    }
+}
+
+// Warp loop over the tiles of one row class: tile indices are grabbed two
+// ahead and row metadata one ahead (software pipeline), so a tile's
+// dependent chain of loads overlaps the previous tile's gathers.
+__device__ void warp_tiles(const LPParams& P, const RoundCtx& R, ClaimCtx& K, BlockCounters& B, WarpTile& T,
+                           double* sw, double* sx, double* sfu, unsigned int* grab, long long nitems, int per,
+                           unsigned long long pol) {
+    const int lane = threadIdx.x & 31;
+    unsigned int kr = 0;
+    if (lane == 0) kr = atomicAdd(grab, (unsigned int)per);
+    long long k = __shfl_sync(0xffffffffu, kr, 0);
+    if (k >= nitems) return;
+    int nr = (int)min((long long)per, nitems - k);
+    TileMeta m = load_meta(P, R, lane < nr ? R.W[k + lane] : -1);
+    if (lane == 0) kr = atomicAdd(grab, (unsigned int)per);
+    for (;;) {
+        const long long kn = __shfl_sync(0xffffffffu, kr, 0);
+        const int nrn = kn < nitems ? (int)min((long long)per, nitems - kn) : 0;
+        const int un = lane < nrn ? R.W[kn + lane] : -1;
+        if (lane == 0 && kn < nitems) kr = atomicAdd(grab, (unsigned int)per);
+        TileMeta mn;
+        warp_tile(P, R, K, B, T, sw, sx, sfu, k, nr, pol, m, un, &mn);
+        __syncwarp();
+        if (kn >= nitems) break;
+        k = kn;
+        nr = nrn;
+        m = mn;
     }
 }
 
@@ -715,23 +760,9 @@ __global__ void __launch_bounds__(kLpThreads, DLP_LP_MINB) k_lp_fused(LPParams P
                 cta_hub_row(P, RH, K, B, smem_dyn, s_fu, k, pol, s_i, s_ll, s_u32);
             }
             RoundCtx RL{W1, n0c, FR, CE, fm_cur, scan_mode};
-            for (;;) {  // long rows: one row per warp tile
-                int k = 0;
-                if (lane == 0) k = (int)atomicAdd(&slot->grab[1], 1u);
-                k = __shfl_sync(0xffffffffu, k, 0);
-                if (k >= n1c) break;
-                warp_tile(P, RL, K, B, T, sw, sx, sfu, k, 1, pol);
-                __syncwarp();
-            }
+            warp_tiles(P, RL, K, B, T, sw, sx, sfu, &slot->grab[1], n1c, 1, pol);  // long rows: one per tile
             RoundCtx RS{W0, 0, FR, CE, fm_cur, scan_mode};
-            for (;;) {  // short rows: rpw rows per warp tile
-                int k = 0;
-                if (lane == 0) k = (int)atomicAdd(&slot->grab[0], (unsigned int)rpw);
-                k = __shfl_sync(0xffffffffu, k, 0);
-                if (k >= n0c) break;
-                warp_tile(P, RS, K, B, T, sw, sx, sfu, k, (int)min((long long)rpw, n0c - k), pol);
-                __syncwarp();
-            }
+            warp_tiles(P, RS, K, B, T, sw, sx, sfu, &slot->grab[0], n0c, rpw, pol);  // short rows
         }
         if (K.claimed) atomicOr(&B.claimed, K.claimed);
         __syncthreads();
@@ -749,16 +780,44 @@ __global__ void __launch_bounds__(kLpThreads, DLP_LP_MINB) k_lp_fused(LPParams P
         grid_sync(&ctl->bar, target);
 
         // ======== phase 2: commit (Jacobi), clear this round's masks ========
-        for (long long i = gtid; i < nwork; i += gth) {
-            int u = i < n0c ? W0[i] : (i < n0c + n1c ? W1[i - n0c] : W2[i - n0c - n1c]);
-            if (ctl->seen) {
-                int old = atomicExch(&ctl->seen[u], (int)(R + 1));
-                if (old == (int)(R + 1)) atomicAdd(&ctl->dups, 1ULL);
+        // two items per thread in flight; full column masks move as 16-byte
+        // vectors (rows of X and of the compact staging are 16-byte aligned
+        // when C is even)
+        for (long long i0 = gtid; i0 < nwork; i0 += 2 * gth) {
+            int uu[2];
+            unsigned int ee[2];
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                const long long i = i0 + h * gth;
+                uu[h] = -1;
+                if (i < nwork) uu[h] = i < n0c ? W0[i] : (i < n0c + n1c ? W1[i - n0c] : W2[i - n0c - n1c]);
             }
-            unsigned int em = P.emask_store[u];
-            for (int c = 0; c < C; c++)
-                if ((em >> c) & 1u) st_keep(P.X + (long long)u * C + c, __ldcs(P.Y + i * C + c), pol);
-            fm_cur[u] = 0;
+#pragma unroll
+            for (int h = 0; h < 2; h++) ee[h] = uu[h] >= 0 ? P.emask_store[uu[h]] : 0u;
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                const long long i = i0 + h * gth;
+                const int u = uu[h];
+                if (u < 0) continue;
+                if (ctl->seen) {
+                    int old = atomicExch(&ctl->seen[u], (int)(R + 1));
+                    if (old == (int)(R + 1)) atomicAdd(&ctl->dups, 1ULL);
+                }
+                const unsigned int em = ee[h];
+                double* xd = P.X + (long long)u * C;
+                const double* yd = P.Y + i * C;
+                if (em == allc && (C & 1) == 0) {
+                    for (int c = 0; c < C; c += 2) {
+                        double2 y = __ldcs((const double2*)(yd + c));
+                        st_keep(xd + c, y.x, pol);
+                        st_keep(xd + c + 1, y.y, pol);
+                    }
+                } else {
+                    for (int c = 0; c < C; c++)
+                        if ((em >> c) & 1u) st_keep(xd + c, __ldcs(yd + c), pol);
+                }
+                fm_cur[u] = 0;
+            }
         }
         if (scan_mode) {
             // compaction of the claimed mask into the next class lists: one
