@@ -61,6 +61,10 @@ constexpr int kLpThreads = 256;
 #ifndef DLP_LP_MINB
 #define DLP_LP_MINB 3
 #endif
+#ifndef DLP_ACC_UNROLL
+#define DLP_ACC_UNROLL 4
+#endif
+constexpr int kAccUnroll = DLP_ACC_UNROLL;  // ordered-sum loop unroll
 constexpr int kWin = DLP_WIN;   // row entries per warp window
 constexpr int kHubWin = DLP_HUB_WIN;  // row entries per CTA window (hub rows)
 constexpr int kLongRow = 96;    // rows longer than this are warp tiles of their own
@@ -407,10 +411,15 @@ __device__ void warp_tile(const LPParams& P, const RoundCtx& R, ClaimCtx& K, Blo
             atomicAdd(&B.uent, (unsigned long long)total);
         }
     }
+#ifdef DLP_SYNC_FU
     for (int i = lane; i < nrows * C; i += 32) {
         int r = i / C, c = i - r * C;
         sfu[i] = ((T.em[r] >> c) & 1u) ? P.X[(long long)T.u[r] * C + c] : 0.0;
     }
+#else
+    // own label rows ride with the first window's asynchronous copies
+    if (lane < nrows && T.em[lane]) copy_label_row(sfu + lane * C, P.X + (long long)T.u[lane] * C, C, pol);
+#endif
     *mn = load_meta(P, R, un);  // next tile's metadata, consumed next iteration
     __syncwarp();
     // ---- accumulate lanes
@@ -419,11 +428,12 @@ __device__ void warp_tile(const LPParams& P, const RoundCtx& R, ClaimCtx& K, Blo
     RowAcc acc;
     acc.init();
     const int a_lo = aact ? T.off[ar] : 0, a_hi = aact ? T.off[ar] + T.len[ar] : 0;
-    for (int wb = 0; wb < total; wb += kWin) {
+    // ids / weights of a window are loaded one window ahead (software pipeline):
+    // a window costs one dependent round trip (the label gathers)
+    int vv[kWin / 32], rr[kWin / 32];
+    double ww[kWin / 32];
+    auto load_ids = [&](int wb) {
         const int wn = min(kWin, total - wb);
-        // gather: kWin/32 entries per lane, all loads independent
-        int vv[kWin / 32], rr[kWin / 32];
-        double ww[kWin / 32];
 #pragma unroll
         for (int j = 0; j < kWin / 32; j++) {
             int i = lane + 32 * j;
@@ -437,6 +447,10 @@ __device__ void warp_tile(const LPParams& P, const RoundCtx& R, ClaimCtx& K, Blo
                 ww[j] = __ldcs(P.w + p);
             }
         }
+    };
+    if (total > 0) load_ids(0);
+    for (int wb = 0; wb < total; wb += kWin) {
+        const int wn = min(kWin, total - wb);
         // label rows: asynchronous copies straight into shared memory, so every
         // gather of the window is in flight at once (no register dependency)
 #pragma unroll
@@ -446,13 +460,19 @@ __device__ void warp_tile(const LPParams& P, const RoundCtx& R, ClaimCtx& K, Blo
             sw[i] = ww[j];
             copy_label_row(sx + i * C, P.X + (long long)vv[j] * C, C, pol);
         }
+        if (wb + kWin < total) load_ids(wb + kWin);
         cp_async_wait_all();
         __syncwarp();
         if (aact) {
             const double fu = sfu[ar * C + ac];
             const int lo = max(a_lo, wb) - wb, hi = min(a_hi, wb + wn) - wb;
+#pragma unroll kAccUnroll
             for (int t = lo; t < hi; t++) acc.add_boxed(sw[t], sx[t * C + ac], fu);
         }
+        __syncwarp();
+    }
+    if (total == 0) {  // no window ran: the own-label copies must still land
+        cp_async_wait_all();
         __syncwarp();
     }
     // ---- finish: stage, count, flag

@@ -6,10 +6,10 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2604_06596_b200 import build  # noqa: E402
 
 VARIANTS = {
-    "w128_h512_b2": ["DLP_WIN=128", "DLP_HUB_WIN=512", "DLP_LP_MINB=2"],
-    "w64_h256_b3": ["DLP_WIN=64", "DLP_HUB_WIN=256", "DLP_LP_MINB=3"],
-    "w64_h256_b4": ["DLP_WIN=64", "DLP_HUB_WIN=256", "DLP_LP_MINB=4"],
-    "w96_h384_b3": ["DLP_WIN=96", "DLP_HUB_WIN=384", "DLP_LP_MINB=3"],
+    "hubw20k": [],
+    "hubw2k": ["DLP_HUB_WARP_ROWS=2000"],
+    "hubw200k": ["DLP_HUB_WARP_ROWS=200000"],
+    "hubcta": ["DLP_HUB_CTA_ALWAYS"],
 }
 if __name__ == "__main__":
     root = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "scratch")
