@@ -489,7 +489,11 @@ def main():
         "survey_model_gbs": survey_bytes / (lp_ms * 1e-3) / 1e9 if lp_ms > 0 else None,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None,
-                     "traffic": (tr or {}).get("dram_bytes_per_alg_byte"),
+                     "traffic": (tr or {}).get("dram_bytes_per_launch"),
+                     "traffic_note": "DRAM read+write bytes of one k_lp_fused launch from an ncu --set full "
+                                     "capture of this workload (profiles/lp_kernel_traffic.json); compare with "
+                                     "algorithmic_bytes_per_launch",
+                     "algorithmic_bytes_per_launch": alg_bytes / K if uent > 0 else None,
                      "kernel": "k_lp_loop (persistent frontier/certify loop)",
                      "algorithmic_bytes": "fused kernel: 20 B/union row + (12 + 8C) B/gathered entry + "
                                           "32 B/(vertex, column) update; see DESIGN.md",

@@ -6,10 +6,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2604_06596_b200 import build  # noqa: E402
 
 VARIANTS = {
-    "hubw20k": [],
-    "hubw2k": ["DLP_HUB_WARP_ROWS=2000"],
-    "hubw200k": ["DLP_HUB_WARP_ROWS=200000"],
-    "hubcta": ["DLP_HUB_CTA_ALWAYS"],
+    "base": [],
+    "l2persist": ["DLP_L2_PERSIST"],
 }
 if __name__ == "__main__":
     root = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "scratch")
