@@ -54,10 +54,12 @@ namespace knn {
 constexpr int BM = 128;           // queries per tile (TMEM lanes)
 constexpr int BN = 256;           // database rows per MMA tile (N)
 constexpr int BKH = 64;           // fp16 elements per K block (128-byte rows)
-constexpr int KP = 32;            // screened candidates kept per (query, split)
+constexpr int KP = 16;            // screened candidates kept per (query, split, column half)
+constexpr int EPI = 2;            // epilogue warpgroups (each drains half of an accumulator)
+constexpr int CH = 16;            // accumulator columns per TMEM load
 constexpr int A_BLOCK = BM * 128;  // bytes of one A K-block slab (16 KB)
 constexpr int B_BLOCK = BN * 128;  // bytes of one B K-block slab (32 KB)
-constexpr int kThreads = 256;
+constexpr int kThreads = 128 + 128 * EPI;
 constexpr int kMaxK = 32;         // largest k served by the screened path
 
 // ---------------------------------------------------------------------------
@@ -184,6 +186,13 @@ __host__ __device__ constexpr unsigned int f16_idesc(int M, int N) {
     return (1u << 4) | (0u << 7) | (0u << 10) | ((unsigned)(N >> 3) << 17) | ((unsigned)(M >> 4) << 24);
 }
 
+#define TMEM_LD16(taddr, r)                                                                                        \
+    asm volatile(                                                                                                  \
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"       \
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),   \
+          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])                      \
+        : "r"(taddr))
+
 #define TMEM_LD32(taddr, r)                                                                                        \
     asm volatile(                                                                                                  \
         "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19," \
@@ -238,11 +247,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_knn_screen(ScreenArgs a) {
     unsigned char* base = (unsigned char*)(((size_t)smem_raw + 1023) & ~(size_t)1023);
     unsigned char* sA = base;
     unsigned char* sB = sA + (size_t)a.KB * A_BLOCK;
-    float* lv = (float*)(sB + (size_t)a.stages * B_BLOCK);  // [KP][128]
-    int* li = (int*)(lv + KP * BM);                         // [KP][128]
-    float* pv = (float*)(li + KP * BM);                     // pending [32][128]
-    int* pi = (int*)(pv + 32 * BM);                         // pending ids
-    unsigned long long* bars = (unsigned long long*)(pi + 32 * BM);
+    // per epilogue group: heap [KP][128] + pending [CH][128] (values, ids)
+    float* epi_base = (float*)(sB + (size_t)a.stages * B_BLOCK);
+    unsigned long long* bars = (unsigned long long*)(epi_base + (size_t)EPI * 2 * (KP + CH) * BM);
     unsigned long long* full = bars;                     // [stages]
     unsigned long long* empty = bars + a.stages;         // [stages]
     unsigned long long* tfull = bars + 2 * a.stages;     // [2]
@@ -260,7 +267,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_knn_screen(ScreenArgs a) {
         }
         for (int s = 0; s < 2; s++) {
             mbar_init(&tfull[s], 1);
-            mbar_init(&tempty[s], BM);
+            mbar_init(&tempty[s], BM * EPI);
         }
         mbar_init(afull, 1);
         mbar_init(aempty, 1);
@@ -349,8 +356,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_knn_screen(ScreenArgs a) {
         }
     } else if (warp >= 4) {
         // ===== epilogue: TMEM -> per-query top-KP candidates =====
-        const int et = tid - 128;  // query row within the tile == TMEM lane
+        // group g drains accumulator columns [g*BN/EPI, (g+1)*BN/EPI) and keeps
+        // its own candidate list per query: list index = split*EPI + g
+        const int g = (warp - 4) >> 2;
+        const int et = (tid - 128) & (BM - 1);  // query row within the tile == TMEM lane
         const unsigned int lane_base = (unsigned int)((warp & 3) * 32) << 16;
+        float* lv = epi_base + (size_t)g * 2 * (KP + CH) * BM;
+        int* li = (int*)(lv + KP * BM);
+        float* pv = (float*)(li + KP * BM);
+        int* pi = (int*)(pv + CH * BM);
+        const int nlist = a.nsplit * EPI;
         int acc = 0;
         unsigned int accph = 0;
         for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
@@ -367,19 +382,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_knn_screen(ScreenArgs a) {
             for (int t = t0; t < t1; t++) {
                 mbar_wait(&tfull[acc], accph);
                 tc_fence_after();
-                for (int j = 0; j < BN / 32; j++) {
-                    unsigned int r[32];
-                    TMEM_LD32(tmem + lane_base + (unsigned int)(acc * BN + j * 32), r);
+                for (int j = 0; j < BN / EPI / CH; j++) {
+                    const int col = g * (BN / EPI) + j * CH;
+                    unsigned int r[CH];
+                    TMEM_LD16(tmem + lane_base + (unsigned int)(acc * BN + col), r);
                     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                    const long long g0 = (long long)t * BN + j * 32;
+                    const long long g0 = (long long)t * BN + col;
                     float mx = __uint_as_float(r[0]);
 #pragma unroll
-                    for (int c = 1; c < 32; c++) mx = fmaxf(mx, __uint_as_float(r[c]));
-                    const bool special = (qid >= g0 && qid < g0 + 32) || g0 + 32 > a.n_db;
+                    for (int c = 1; c < CH; c++) mx = fmaxf(mx, __uint_as_float(r[c]));
+                    const bool special = (qid >= g0 && qid < g0 + CH) || g0 + CH > a.n_db;
                     if (!__any_sync(0xffffffffu, mx > thr || special)) continue;
                     int pc = 0;
 #pragma unroll
-                    for (int c = 0; c < 32; c++) {
+                    for (int c = 0; c < CH; c++) {
                         const float v = __uint_as_float(r[c]);
                         const long long gid = g0 + c;
                         const bool pass = v > thr && gid < a.n_db && gid != qid;
@@ -415,12 +431,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_knn_screen(ScreenArgs a) {
                 }
             }
             if (qrow < a.nq) {
-                const size_t o = ((size_t)qrow * a.nsplit + split) * KP;
-                for (int s = 0; s < KP; s++) {
-                    a.cand_val[o + s] = s < cnt ? lv[s * BM + et] : -INFINITY;
-                    a.cand_id[o + s] = s < cnt ? li[s * BM + et] : -1;
+                const int list = split * EPI + g;
+                const size_t o = ((size_t)qrow * nlist + list) * KP;
+                for (int s2 = 0; s2 < KP; s2++) {
+                    a.cand_val[o + s2] = s2 < cnt ? lv[s2 * BM + et] : -INFINITY;
+                    a.cand_id[o + s2] = s2 < cnt ? li[s2 * BM + et] : -1;
                 }
-                a.cand_min[(size_t)qrow * a.nsplit + split] = cnt < KP ? -INFINITY : thr;
+                a.cand_min[(size_t)qrow * nlist + list] = cnt < KP ? -INFINITY : thr;
             }
         }
     }
@@ -714,9 +731,6 @@ int run_queries(dlp_knn* h, long long q0, long long nq, int k) {
         int nsplit = choose_nsplit(nqt, n_btiles, h->sm_count);
         const int tps = (n_btiles + nsplit - 1) / nsplit;
         nsplit = (n_btiles + tps - 1) / tps;
-        h->cand_val.reserve((size_t)nq * nsplit * KP, 0, st);
-        h->cand_id.reserve((size_t)nq * nsplit * KP, 0, st);
-        h->cand_min.reserve((size_t)nq * nsplit, 0, st);
         ScreenArgs a;
         a.opA = h->opA.p + (size_t)(q0 / BM) * h->KB * A_BLOCK;
         a.opB = h->opB.p;
@@ -730,14 +744,15 @@ int run_queries(dlp_knn* h, long long q0, long long nq, int k) {
         a.nsplit = nsplit;
         a.tiles_per_split = tps;
         a.nqt = (int)((a.nq + BM - 1) / BM);
-        const size_t fixed = (size_t)h->KB * A_BLOCK + (size_t)(KP + 32) * BM * 8 + 1024 + 256;
+        const size_t fixed = (size_t)h->KB * A_BLOCK + (size_t)EPI * (KP + CH) * BM * 8 + 1024 + 256;
         const size_t limit = 227 * 1024;
         a.stages = (int)std::min<size_t>(8, (limit - fixed) / B_BLOCK);
         if (a.stages < 2) return kfail(h, DLP_EVALIDATION, "feature dimension too large for the tensor-core screen");
         // candidate buffers are indexed by the padded query row
-        h->cand_val.reserve((size_t)a.nq * nsplit * KP, 0, st);
-        h->cand_id.reserve((size_t)a.nq * nsplit * KP, 0, st);
-        h->cand_min.reserve((size_t)a.nq * nsplit, 0, st);
+        const int nlist = nsplit * EPI;
+        h->cand_val.reserve((size_t)a.nq * nlist * KP, 0, st);
+        h->cand_id.reserve((size_t)a.nq * nlist * KP, 0, st);
+        h->cand_min.reserve((size_t)a.nq * nlist, 0, st);
         a.cand_val = h->cand_val.p;
         a.cand_id = h->cand_id.p;
         a.cand_min = h->cand_min.p;
@@ -749,8 +764,8 @@ int run_queries(dlp_knn* h, long long q0, long long nq, int k) {
         DLP_CUDA_TRY(cudaEventRecord(h->tev[1], st));
         // --- exact re-check with certificate
         k_knn_recheck<<<blocks_for(nq * 32, 256, 148 * 16), 256, 0, st>>>(
-            h->xn.p, D, q0, nq, nsplit, k, h->cand_val.p + (size_t)qpad * nsplit * KP,
-            h->cand_id.p + (size_t)qpad * nsplit * KP, h->cand_min.p + (size_t)qpad * nsplit, h->eps, h->top_id.p,
+            h->xn.p, D, q0, nq, nlist, k, h->cand_val.p + (size_t)qpad * nlist * KP,
+            h->cand_id.p + (size_t)qpad * nlist * KP, h->cand_min.p + (size_t)qpad * nlist, h->eps, h->top_id.p,
             h->top_sim.p, h->failed.p, h->counters.p);
         DLP_CUDA_TRY(cudaGetLastError());
         DLP_CUDA_TRY(cudaEventRecord(h->tev[2], st));
@@ -1057,14 +1072,15 @@ int dlp_knn_debug_candidates(dlp_knn* h, int64_t q0, int64_t q1, int32_t* nsplit
         int nsplit = choose_nsplit(nqt, n_btiles, h->sm_count);
         const int tps = (n_btiles + nsplit - 1) / nsplit;
         nsplit = (n_btiles + tps - 1) / tps;
-        *nsplit_out = nsplit;
-        if ((long long)nq * nsplit * KP > cap) return kfail(h, DLP_EVALIDATION, "capacity too small");
+        const int nlist = nsplit * EPI;
+        *nsplit_out = nlist;  // candidate lists per query, KP each
+        if ((long long)nq * nlist * KP > cap) return kfail(h, DLP_EVALIDATION, "capacity too small");
         const long long qpad = q0 - (q0 / BM) * BM;
-        DLP_CUDA_TRY(cudaMemcpy(val, h->cand_val.p + (size_t)qpad * nsplit * KP, (size_t)nq * nsplit * KP * 4,
+        DLP_CUDA_TRY(cudaMemcpy(val, h->cand_val.p + (size_t)qpad * nlist * KP, (size_t)nq * nlist * KP * 4,
                                 cudaMemcpyDeviceToHost));
-        DLP_CUDA_TRY(cudaMemcpy(id, h->cand_id.p + (size_t)qpad * nsplit * KP, (size_t)nq * nsplit * KP * 4,
+        DLP_CUDA_TRY(cudaMemcpy(id, h->cand_id.p + (size_t)qpad * nlist * KP, (size_t)nq * nlist * KP * 4,
                                 cudaMemcpyDeviceToHost));
-        DLP_CUDA_TRY(cudaMemcpy(thr, h->cand_min.p + (size_t)qpad * nsplit, (size_t)nq * nsplit * 4,
+        DLP_CUDA_TRY(cudaMemcpy(thr, h->cand_min.p + (size_t)qpad * nlist, (size_t)nq * nlist * 4,
                                 cudaMemcpyDeviceToHost));
     } catch (const CudaFailure& f) {
         h->err = std::string("CUDA error: ") + cudaGetErrorString(f.err);

@@ -117,17 +117,20 @@ class KnnIndex:
                                             C.byref(e)))
         return KnnStats(a.value, b.value, c.value, nf.value, nq.value, e.value)
 
+    KP = 16  # candidates per list (csrc/knn.cu)
+
     def debug_candidates(self, q0: int, q1: int):
+        """Screened candidates of the last query call: (lists, val, id, thr)."""
         nq = q1 - q0
-        cap = nq * 16 * 32
+        cap = nq * 64 * self.KP
         ns = C.c_int32()
         val = np.empty(cap, dtype=np.float32)
         ids = np.empty(cap, dtype=np.int32)
-        thr = np.empty(nq * 16, dtype=np.float32)
+        thr = np.empty(nq * 64, dtype=np.float32)
         self._check(self._lib.dlp_knn_debug_candidates(self._h, q0, q1, C.byref(ns), val.ctypes.data,
                                                        ids.ctypes.data, thr.ctypes.data, cap))
-        s = ns.value
-        return s, val[:nq * s * 32].reshape(nq, s * 32), ids[:nq * s * 32].reshape(nq, s * 32), \
+        s, kp = ns.value, self.KP
+        return s, val[:nq * s * kp].reshape(nq, s * kp), ids[:nq * s * kp].reshape(nq, s * kp), \
             thr[:nq * s].reshape(nq, s)
 
 
