@@ -529,6 +529,7 @@ __device__ void warp_tiles(const LPParams& P, const RoundCtx& R, ClaimCtx& K, Bl
                            double* sw, double* sx, double* sfu, unsigned int* grab, long long nitems, int per,
                            unsigned long long pol) {
     const int lane = threadIdx.x & 31;
+    if (nitems <= 0) return;
     unsigned int kr = 0;
     if (lane == 0) kr = atomicAdd(grab, (unsigned int)per);
     long long k = __shfl_sync(0xffffffffu, kr, 0);
@@ -740,6 +741,8 @@ __global__ void __launch_bounds__(kLpThreads, DLP_LP_MINB) k_lp_fused(LPParams P
 
     long long R = resume ? ctl->r_par : 0;
     while (!S.done) {
+        unsigned long long t_r0 = 0, t_p1 = 0;
+        if (ctl->trace && gtid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_r0));
         const unsigned int FR = S.fr_mask, CE = S.cert_mask;
         const int ri = (int)(R & 1), rn = ri ^ 1;
         RoundSlot* slot = &ctl->slot[ri];
@@ -771,13 +774,15 @@ __global__ void __launch_bounds__(kLpThreads, DLP_LP_MINB) k_lp_fused(LPParams P
         // staging items: short [0, n0c), long [n0c, n0c+n1c), hub [n0c+n1c, nwork)
         {
             RoundCtx RH{W2, n0c + n1c, FR, CE, fm_cur, scan_mode};
-            for (;;) {  // hub rows: whole CTA per row (critical path first)
-                if (tid == 0) s_i[2] = (int)atomicAdd(&slot->grab[2], 1u);
-                __syncthreads();
-                const int k = s_i[2];
-                __syncthreads();
-                if (k >= n2c) break;
-                cta_hub_row(P, RH, K, B, smem_dyn, s_fu, k, pol, s_i, s_ll, s_u32);
+            if (n2c > 0) {
+                for (;;) {  // hub rows: whole CTA per row (critical path first)
+                    if (tid == 0) s_i[2] = (int)atomicAdd(&slot->grab[2], 1u);
+                    __syncthreads();
+                    const int k = s_i[2];
+                    __syncthreads();
+                    if (k >= n2c) break;
+                    cta_hub_row(P, RH, K, B, smem_dyn, s_fu, k, pol, s_i, s_ll, s_u32);
+                }
             }
             RoundCtx RL{W1, n0c, FR, CE, fm_cur, scan_mode};
             warp_tiles(P, RL, K, B, T, sw, sx, sfu, &slot->grab[1], n1c, 1, pol);  // long rows: one per tile
@@ -798,6 +803,7 @@ __global__ void __launch_bounds__(kLpThreads, DLP_LP_MINB) k_lp_fused(LPParams P
             if (B.uent) atomicAdd(&slot->uentries, B.uent);
         }
         grid_sync(&ctl->bar, target);
+        if (ctl->trace && gtid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_p1));
 
         // ======== phase 2: commit (Jacobi), clear this round's masks ========
         // two items per thread in flight; full column masks move as 16-byte
@@ -932,7 +938,9 @@ __global__ void __launch_bounds__(kLpThreads, DLP_LP_MINB) k_lp_fused(LPParams P
         if (ctl->trace && gtid == 0 && R < ctl->trace_cap) {
             unsigned long long t;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-            unsigned long long* e = ctl->trace + 4 * R;
+            unsigned long long* e = ctl->trace + 8 * R;
+            e[4] = t_p1;
+            e[5] = t_r0;
             e[0] = (unsigned long long)n0c;
             e[1] = (unsigned long long)(n1c + (n2c << 32));
             e[2] = (unsigned long long)FR | ((unsigned long long)CE << 16) | ((unsigned long long)scan_mode << 32);
@@ -1042,7 +1050,7 @@ void lp_run_dev(Engine& E, double delta, long long max_iter, bool itlp) {
     DLP_CUDA_TRY(cudaMemsetAsync(E.ctl, 0, sizeof(LPCtl), E.st));
     if (E.lp_trace_path) {
         const long long cap = 1 << 16;
-        E.lp_trace.reserve(4 * cap + 4, 0, E.st);
+        E.lp_trace.reserve(8 * cap + 8, 0, E.st);
         unsigned long long* tp = E.lp_trace.p;
         DLP_CUDA_TRY(cudaMemcpyAsync(&E.ctl->trace, &tp, sizeof(tp), cudaMemcpyHostToDevice, E.st));
         DLP_CUDA_TRY(cudaMemcpyAsync(&E.ctl->trace_cap, &cap, sizeof(cap), cudaMemcpyHostToDevice, E.st));
@@ -1110,13 +1118,14 @@ void lp_run_actions(Engine& E, double delta, bool first, bool cleanup) {
 void lp_dump_trace(Engine& E, long long rounds) {
     if (!E.lp_trace_path || rounds <= 0) return;
     long long n = std::min<long long>(rounds, 1 << 16);
-    std::vector<unsigned long long> h(4 * n);
+    std::vector<unsigned long long> h(8 * n);
     DLP_CUDA_TRY(cudaMemcpy(h.data(), E.lp_trace.p, h.size() * 8, cudaMemcpyDeviceToHost));
     FILE* fp = fopen(E.lp_trace_path, "a");
     if (!fp) return;
     fprintf(fp, "# launch rounds=%lld grid=%d dups=%llu\n", rounds, E.lp_grid, E.h_ctl.p->dups);
     for (long long r = 0; r < n; r++)
-        fprintf(fp, "%lld %llu %llu %llx %llu\n", r, h[4 * r], h[4 * r + 1], h[4 * r + 2], h[4 * r + 3]);
+        fprintf(fp, "%lld %llu %llu %llx %llu %llu %llu\n", r, h[8 * r], h[8 * r + 1], h[8 * r + 2], h[8 * r + 3],
+                h[8 * r + 4], h[8 * r + 5]);
     fclose(fp);
 }
 

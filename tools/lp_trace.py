@@ -13,8 +13,10 @@ def launches(path):
                 out.append(np.array(cur, dtype=np.float64))
             cur = []
             continue
-        r, ns, nl, m, t = ln.split()
-        cur.append((int(r), int(ns), int(nl), int(m, 16), int(t)))
+        f = ln.split()
+        r, ns, nl, m, t = f[:5]
+        p1, r0 = (int(f[5]), int(f[6])) if len(f) >= 7 else (0, 0)
+        cur.append((int(r), int(ns), int(nl), int(m, 16), int(t), p1, r0))
     if cur:
         out.append(np.array(cur, dtype=np.float64))
     return out
@@ -36,6 +38,15 @@ def summarise(a):
         if m.any():
             print(f"  frontier rows [{lo:.0e},{hi:.0e}): rounds={m.sum()} ms={dt[m].sum() / 1e3:.2f} "
                   f"us/round={dt[m].mean():.1f} rows/us={rows[m].sum() / max(dt[m].sum(), 1e-9):.0f}")
+    if a.shape[1] >= 7 and a[0, 5] > 0:
+        ph1 = (a[:, 5] - a[:, 6]) / 1e3
+        rest = (a[:, 4] - a[:, 5]) / 1e3
+        gap = np.concatenate([[0.0], (a[1:, 6] - a[:-1, 4]) / 1e3])
+        for lo, hi in [(0, 1e3), (1e3, 1e4), (1e4, 1e5), (1e5, 1e7)]:
+            sel = (~ce) & (rows >= lo) & (rows < hi)
+            if sel.any():
+                print(f"    rows [{lo:.0e},{hi:.0e}): phase1 {ph1[sel].mean():.1f} us, commit+controller "
+                      f"{rest[sel].mean():.1f} us, inter-round {gap[sel].mean():.1f} us")
     if ce.any():
         print(f"  certify: us/round={dt[ce].mean():.1f} rows/round={rows[ce].mean():.0f} "
               f"long/round={nlong[ce].mean():.0f} hub/round={nhub[ce].mean():.0f}")
