@@ -151,8 +151,16 @@ __device__ inline void cp_async8(double* dst, const double* src, unsigned long l
 }
 __device__ inline void cp_async16(double* dst, const double* src, unsigned long long pol) {
     unsigned int d = (unsigned int)__cvta_generic_to_shared(dst);
+#ifdef DLP_CP_CA
+    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "l"(pol)
+                 : "memory");
+#elif defined(DLP_CP_NOHINT)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+    (void)pol;
+#else
     asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "l"(pol)
                  : "memory");
+#endif
 }
 __device__ inline void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
@@ -552,6 +560,278 @@ __device__ void warp_tiles(const LPParams& P, const RoundCtx& R, ClaimCtx& K, Bl
     }
 }
 
+// ---------------------------------------------------------------------------
+// Producer / consumer warp pairs (DLP_PC): warps 0-3 only gather, warps 4-7
+// only sum.  A producer takes tiles (same tiles as warp_tiles), stages each
+// 64-entry chunk -- row metadata, ids, weights and the label vectors by
+// cp.async -- into a 2-slot ring shared with its consumer and signals the
+// slot's mbarrier when the copies land (cp.async.mbarrier.arrive.noinc), so
+// it can move on to the next chunk's id loads at once; the consumer runs the
+// ordered sums, finishes the rows and expands.  Memory and the dependent
+// fp64 chains overlap instead of alternating inside one warp.
+// ---------------------------------------------------------------------------
+constexpr int PC_FIRST = 1, PC_LAST = 2, PC_DONE = 4;
+constexpr int kPCSlots = 2;
+
+__host__ __device__ inline size_t pc_slot_bytes(int C) {
+    size_t b = 64 + 4 * (32 + 32 + 40 + 32) + 8 * 32 + 8 * 32 + 4 * (size_t)kWin + 8 * (size_t)kWin +
+               8 * (size_t)kWin * C;
+    return (b + 127) & ~(size_t)127;
+}
+
+struct PCSlot {
+    int* hdr;  // nrows, e0, e1, flags, total
+    long long* ybase;
+    int *u, *off, *len;
+    unsigned int* em;
+    long long* st;
+    double* fu;
+    int* nbr;
+    double *w, *x;
+};
+
+__device__ inline PCSlot pc_slot(unsigned char* base) {
+    PCSlot s;
+    s.hdr = (int*)base;
+    s.ybase = (long long*)(base + 32);
+    s.u = (int*)(base + 64);
+    s.em = (unsigned int*)(s.u + 32);
+    s.off = (int*)(s.em + 32);
+    s.len = s.off + 40;
+    s.st = (long long*)(s.len + 32);
+    s.fu = (double*)(s.st + 32);
+    s.nbr = (int*)(s.fu + 32);
+    s.w = (double*)(s.nbr + kWin);
+    s.x = s.w + kWin;
+    return s;
+}
+
+__device__ inline void mbar_init_s(unsigned long long* b, unsigned int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned int)__cvta_generic_to_shared(b)),
+                 "r"(count)
+                 : "memory");
+}
+__device__ inline void mbar_arrive_s(unsigned long long* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"((unsigned int)__cvta_generic_to_shared(b))
+                 : "memory");
+}
+__device__ inline void mbar_arrive_cp(unsigned long long* b) {  // when this thread's cp.asyncs land
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(
+                     (unsigned int)__cvta_generic_to_shared(b))
+                 : "memory");
+}
+__device__ inline void mbar_wait_s(unsigned long long* b, unsigned int parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "PCW_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra PCW_%=;\n}" ::"r"((unsigned int)__cvta_generic_to_shared(b)),
+        "r"(parity)
+        : "memory");
+}
+
+struct PCRing {
+    unsigned char* base;  // kPCSlots slots of pc_slot_bytes(C)
+    unsigned long long* full;
+    unsigned long long* empty;
+    size_t sb;
+    int s;
+    unsigned int ph;
+    __device__ inline unsigned char* cur() const { return base + (size_t)s * sb; }
+    __device__ inline void advance() {
+        if (++s == kPCSlots) {
+            s = 0;
+            ph ^= 1;
+        }
+    }
+};
+
+// producer: stage every chunk of the tiles of one row class
+__device__ void pc_produce_class(const LPParams& P, const RoundCtx& R, unsigned int* grab, long long nitems, int per,
+                                 PCRing& ring, unsigned long long pol) {
+    const int C = P.C;
+    const int lane = threadIdx.x & 31;
+    if (nitems <= 0) return;
+    unsigned int kr = 0;
+    if (lane == 0) kr = atomicAdd(grab, (unsigned int)per);
+    long long k = __shfl_sync(0xffffffffu, kr, 0);
+    if (k >= nitems) return;
+    int nr = (int)min((long long)per, nitems - k);
+    TileMeta m = load_meta(P, R, lane < nr ? R.W[k + lane] : -1);
+    if (lane == 0) kr = atomicAdd(grab, (unsigned int)per);
+    for (;;) {
+        const long long kn = __shfl_sync(0xffffffffu, kr, 0);
+        const int nrn = kn < nitems ? (int)min((long long)per, nitems - kn) : 0;
+        const int un = lane < nrn ? R.W[kn + lane] : -1;
+        if (lane == 0 && kn < nitems) kr = atomicAdd(grab, (unsigned int)per);
+        // ---- tile k: rows in registers, offsets by a warp scan
+        unsigned int em = 0;
+        int len = 0;
+        long long st = 0;
+        if (lane < nr) {
+            em = m.em;
+            P.emask_store[m.u] = em;
+            len = em ? m.len : 0;
+            st = em ? m.st : 0;
+        }
+        int incl = len;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const int off = incl - len;
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        TileMeta mn = load_meta(P, R, un);  // next tile's metadata, consumed next iteration
+        const int nch = total > 0 ? (total + kWin - 1) / kWin : 1;
+        for (int ch = 0; ch < nch; ch++) {
+            const int e0 = ch * kWin, e1 = min(total, e0 + kWin);
+            mbar_wait_s(&ring.empty[ring.s], ring.ph ^ 1);
+            PCSlot S = pc_slot(ring.cur());
+            if (lane == 0) {
+                S.hdr[0] = nr;
+                S.hdr[1] = e0;
+                S.hdr[2] = e1;
+                S.hdr[3] = (ch == 0 ? PC_FIRST : 0) | (ch == nch - 1 ? PC_LAST : 0);
+                S.hdr[4] = total;
+                *S.ybase = R.ybase + k;
+            }
+            if (lane < nr) {
+                S.u[lane] = m.u;
+                S.em[lane] = em;
+                S.off[lane] = off;
+                S.len[lane] = len;
+                S.st[lane] = st;
+                if (ch == 0 && em) copy_label_row(S.fu + lane * C, P.X + (long long)m.u * C, C, pol);
+            }
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j < kWin / 32; j++) {
+                const int i = lane + 32 * j;
+                if (i < e1 - e0) {
+                    const int g = e0 + i;
+                    const int r = tile_row_of(S.off, nr, g);
+                    const long long p = S.st[r] + (g - S.off[r]);
+                    const int v = __ldcs(P.nbr + p);
+                    S.nbr[i] = v;
+                    S.w[i] = __ldcs(P.w + p);
+                    copy_label_row(S.x + i * C, P.X + (long long)v * C, C, pol);
+                }
+            }
+            __syncwarp();
+            mbar_arrive_cp(&ring.full[ring.s]);
+            if (lane == 0) mbar_arrive_s(&ring.full[ring.s]);
+            ring.advance();
+        }
+        if (kn >= nitems) break;
+        k = kn;
+        nr = nrn;
+        m = mn;
+    }
+}
+
+__device__ void pc_produce_done(PCRing& ring) {
+    const int lane = threadIdx.x & 31;
+    mbar_wait_s(&ring.empty[ring.s], ring.ph ^ 1);
+    PCSlot S = pc_slot(ring.cur());
+    if (lane == 0) S.hdr[3] = PC_DONE;
+    __syncwarp();
+    mbar_arrive_cp(&ring.full[ring.s]);
+    if (lane == 0) mbar_arrive_s(&ring.full[ring.s]);
+    ring.advance();
+}
+
+// consumer: ordered sums, finish and expand for every staged chunk
+__device__ void pc_consume(const LPParams& P, bool scan_mode, ClaimCtx& K, BlockCounters& B, PCRing& ring) {
+    const int C = P.C;
+    const int lane = threadIdx.x & 31;
+    const int ar = lane / C, ac = lane - ar * C;
+    RowAcc acc;
+    bool aact = false;
+    double fu = 0.0;
+    int a_lo = 0, a_hi = 0;
+    for (;;) {
+        mbar_wait_s(&ring.full[ring.s], ring.ph);
+        PCSlot S = pc_slot(ring.cur());
+        const int flags = S.hdr[3];
+        if (flags & PC_DONE) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive_s(&ring.empty[ring.s]);
+            ring.advance();
+            break;
+        }
+        const int nr = S.hdr[0], e0 = S.hdr[1], e1 = S.hdr[2];
+        if (flags & PC_FIRST) {
+            aact = ar < nr && ((S.em[ar] >> ac) & 1u);
+            acc.init();
+            a_lo = aact ? S.off[ar] : 0;
+            a_hi = aact ? S.off[ar] + S.len[ar] : 0;
+            fu = aact ? S.fu[ar * C + ac] : 0.0;
+        }
+        if (aact) {
+            const int lo = max(a_lo, e0) - e0, hi = min(a_hi, e1) - e0;
+#pragma unroll kAccUnroll
+            for (int t = lo; t < hi; t++) acc.add_boxed(S.w[t], S.x[t * C + ac], fu);
+        }
+        if (flags & PC_LAST) {
+            unsigned int ch = 0;
+            if (aact) {
+                const int u = S.u[ar];
+                double val;
+                double d = acc.finish(fu, &val);
+                __stcs(P.Y + (*S.ybase + ar) * C + ac, val);
+                atomicAdd(&B.neval[ac], 1ULL);
+                atomicAdd(&B.edges[ac], (unsigned long long)S.len[ar]);
+                if (d < 0.0) {  // isolated sentinel (_csr.pyx:49-51, 170-173)
+                    atomicAdd(&B.warn[ac], 1ULL);
+                    atomicAnd(&P.eligm[u], ~(1u << ac));
+                    atomicAdd((unsigned long long*)&P.ctl->elig_count[ac], ~0ULL);
+                } else {
+                    if (d > 0.0) atomicMax(&B.rmax[ac], dbits(d));
+                    if (!P.itlp && d > P.delta) ch = 1u << ac;
+                }
+            }
+            {
+                unsigned int nz = __ballot_sync(0xffffffffu, lane < nr && S.em[lane] != 0);
+                if (lane == 0 && nz) {
+                    atomicAdd(&B.urows, (unsigned long long)__popc(nz));
+                    atomicAdd(&B.uent, (unsigned long long)S.hdr[4]);
+                }
+            }
+            if (!P.itlp) {
+                const unsigned int bal = __ballot_sync(0xffffffffu, ch != 0);
+                if (bal) {
+                    const unsigned int cmask = C >= 32 ? 0xffffffffu : ((1u << C) - 1u);
+                    const int total = S.hdr[4];
+                    if (lane < nr) {
+                        unsigned int mm = (bal >> (lane * C)) & cmask;
+                        if (mm) {
+                            K.claimed |= mm;
+                            if (scan_mode)
+                                atomicOr(&K.fm_next[S.u[lane]], mm);
+                            else
+                                claim(K, S.u[lane], mm);
+                        }
+                    }
+                    for (int g = lane; g < total; g += 32) {
+                        int r = tile_row_of(S.off, nr, g);
+                        unsigned int mm = (bal >> (r * C)) & cmask;
+                        if (!mm) continue;
+                        int v = __ldcs(P.nbr + S.st[r] + (g - S.off[r]));
+                        if (scan_mode)
+                            atomicOr(&K.fm_next[v], mm);
+                        else
+                            claim(K, v, mm);
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive_s(&ring.empty[ring.s]);
+        ring.advance();
+    }
+}
+
 // Hub row (row_len > kHubRow) evaluated by the whole CTA: windows of
 // kHubWin entries are gathered by warps 1..7 (product terms precomputed)
 // into a double buffer while warp 0 (one lane per column) runs the ordered
@@ -662,6 +942,9 @@ __global__ void __launch_bounds__(kLpThreads, DLP_LP_MINB) k_lp_fused(LPParams P
     __shared__ int s_i[4];
     __shared__ unsigned int s_u32[4], s_claimed, s_cnt[3], s_base[3];
     __shared__ unsigned int s_wc[3][kLpThreads / 32];
+#ifdef DLP_PC
+    __shared__ unsigned long long pc_full[4][kPCSlots], pc_empty[4][kPCSlots];
+#endif
 
     const int C = P.C;
     const int tid = threadIdx.x;
@@ -680,6 +963,19 @@ __global__ void __launch_bounds__(kLpThreads, DLP_LP_MINB) k_lp_fused(LPParams P
     const int rpw = 32 / C;  // rows per short tile
     const long long n = P.n;
 
+#ifdef DLP_PC
+    if (tid == 0) {
+        for (int p = 0; p < 4; p++)
+            for (int q = 0; q < kPCSlots; q++) {
+                mbar_init_s(&pc_full[p][q], 33);
+                mbar_init_s(&pc_empty[p][q], 1);
+            }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    PCRing ring{(unsigned char*)smem_dyn + (size_t)(warp & 3) * kPCSlots * pc_slot_bytes(C), pc_full[warp & 3],
+                pc_empty[warp & 3], pc_slot_bytes(C), 0, 0u};
+#endif
     // ---- prologue: F0 (engine.py:364-367) is every column's first frontier;
     // the eligible list and F0 are split by row class.  In action mode only
     // the first launch of a batch runs it; later launches resume the lists.
@@ -785,9 +1081,20 @@ __global__ void __launch_bounds__(kLpThreads, DLP_LP_MINB) k_lp_fused(LPParams P
                 }
             }
             RoundCtx RL{W1, n0c, FR, CE, fm_cur, scan_mode};
-            warp_tiles(P, RL, K, B, T, sw, sx, sfu, &slot->grab[1], n1c, 1, pol);  // long rows: one per tile
             RoundCtx RS{W0, 0, FR, CE, fm_cur, scan_mode};
+#ifdef DLP_PC
+            if (warp < 4) {
+                pc_produce_class(P, RL, &slot->grab[1], n1c, 1, ring, pol);  // long rows: one per tile
+                pc_produce_class(P, RS, &slot->grab[0], n0c, rpw, ring, pol);  // short rows
+                pc_produce_done(ring);
+            } else {
+                pc_consume(P, scan_mode, K, B, ring);
+            }
+            (void)T;
+#else
+            warp_tiles(P, RL, K, B, T, sw, sx, sfu, &slot->grab[1], n1c, 1, pol);  // long rows: one per tile
             warp_tiles(P, RS, K, B, T, sw, sx, sfu, &slot->grab[0], n0c, rpw, pol);  // short rows
+#endif
         }
         if (K.claimed) atomicOr(&B.claimed, K.claimed);
         __syncthreads();
@@ -997,6 +1304,9 @@ void lp_setup(Engine& E) {
     if (E.ncol > kMaxCols) throw CudaFailure(cudaErrorInvalidValue, "ncol > kMaxCols", __FILE__, __LINE__);
     E.lp_smem = std::max((size_t)(kLpThreads / 32) * (kWin * (E.ncol + 1) + 32),
                          (size_t)2 * kHubWin * (E.ncol + 1)) * sizeof(double);
+#ifdef DLP_PC
+    E.lp_smem = std::max(E.lp_smem, (size_t)4 * kPCSlots * pc_slot_bytes(E.ncol));
+#endif
     DLP_CUDA_TRY(cudaFuncSetAttribute(k_lp_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)E.lp_smem));
     int occ = 0;
     DLP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_lp_fused, kLpThreads, E.lp_smem));

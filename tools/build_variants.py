@@ -6,8 +6,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2604_06596_b200 import build  # noqa: E402
 
 VARIANTS = {
-    "base": [],
-    "l2persist": ["DLP_L2_PERSIST"],
+    "ca": ["DLP_CP_CA"],
+    "nohint": ["DLP_CP_NOHINT"],
+    "pc_ca": ["DLP_PC", "DLP_CP_CA"],
 }
 if __name__ == "__main__":
     root = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "scratch")
