@@ -85,6 +85,7 @@ struct LPCtl {
     unsigned long long* trace;
     long long trace_cap;
     int* seen;               // debug: per-vertex round stamp (duplicate work items)
+    unsigned long long* prof; // diagnostics: warp-ns in hub / long / short parts of phase 1
     unsigned long long dups; // debug: duplicate work items detected
     // ---- action mode (component-sharded execution): the host
     // runs each column's engine.py:375-405 state machine on phase results
@@ -213,6 +214,7 @@ struct Engine {
     int lp_grid = 0;
     DevArray<unsigned long long> lp_trace;
     DevArray<int> lp_seen;
+    DevArray<unsigned long long> lp_prof;
     const char* lp_trace_path = nullptr;
     size_t lp_smem = 0;
     // instrumentation: kernel launches issued and LP kernel time per column

@@ -68,7 +68,10 @@ constexpr int kAccUnroll = DLP_ACC_UNROLL;  // ordered-sum loop unroll
 constexpr int kWin = DLP_WIN;   // row entries per warp window
 constexpr int kHubWin = DLP_HUB_WIN;  // row entries per CTA window (hub rows)
 constexpr int kLongRow = 96;    // rows longer than this are warp tiles of their own
-constexpr int kHubRow = 384;    // rows longer than this are evaluated by a whole CTA
+#ifndef DLP_HUB_ROW_DEFAULT
+#define DLP_HUB_ROW_DEFAULT 384
+#endif
+constexpr int kHubRow = DLP_HUB_ROW_DEFAULT;  // rows longer than this are evaluated by a whole CTA
 constexpr int kScanRatio = 64;  // rounds with >= n/64 rows expand by atomicOr + compaction
 
 enum { PH_FRONTIER = 0, PH_DONE = 2 };
@@ -474,8 +477,37 @@ __device__ void warp_tile(const LPParams& P, const RoundCtx& R, ClaimCtx& K, Blo
         if (aact) {
             const double fu = sfu[ar * C + ac];
             const int lo = max(a_lo, wb) - wb, hi = min(a_hi, wb + wn) - wb;
+#ifdef DLP_GT_SPLIT
+            // The four sums are independent chains: w_all and s over the window
+            // here (a ground-truth entry adds (fu - fu) * w = +0.0 to s, which is
+            // bit-neutral), w0 / w1 only over the rare ground-truth entries in a
+            // second ordered pass -- each chain still sees its entries in row order.
+            bool any_gt = false;
+            double s_ = acc.s, wa = acc.w_all;
+#pragma unroll kAccUnroll
+            for (int t = lo; t < hi; t++) {
+                const double w = sw[t], x = sx[t * C + ac];
+                const bool g = is_boxed(x);
+                any_gt |= g;
+                wa = __dadd_rn(wa, w);
+                s_ = __dadd_rn(s_, __dmul_rn(__dsub_rn(g ? fu : x, fu), w));
+            }
+            acc.s = s_;
+            acc.w_all = wa;
+            if (any_gt) {
+                for (int t = lo; t < hi; t++) {
+                    const double x = sx[t * C + ac];
+                    if (!is_boxed(x)) continue;
+                    if (boxed_class(x) == 0)
+                        acc.w0 = __dadd_rn(acc.w0, sw[t]);
+                    else
+                        acc.w1 = __dadd_rn(acc.w1, sw[t]);
+                }
+            }
+#else
 #pragma unroll kAccUnroll
             for (int t = lo; t < hi; t++) acc.add_boxed(sw[t], sx[t * C + ac], fu);
+#endif
         }
         __syncwarp();
     }
@@ -517,6 +549,20 @@ __device__ void warp_tile(const LPParams& P, const RoundCtx& R, ClaimCtx& K, Blo
             else
                 claim(K, T.u[lane], m);
         }
+    }
+    if (total <= kWin) {
+        // single-window tile: the gathering lanes still hold the entries' ids
+#pragma unroll
+        for (int j = 0; j < kWin / 32; j++) {
+            if (rr[j] < 0) continue;
+            const unsigned int m = (bal >> (rr[j] * C)) & cmask;
+            if (!m) continue;
+            if (R.scan_mode)
+                atomicOr(&K.fm_next[vv[j]], m);  // no return value: a fire-and-forget RED
+            else
+                claim(K, vv[j], m);
+        }
+        return;
     }
     for (int g = lane; g < total; g += 32) {
         int r = tile_row_of(T.off, nrows, g);
@@ -1066,10 +1112,15 @@ __global__ void __launch_bounds__(kLpThreads, DLP_LP_MINB) k_lp_fused(LPParams P
         }
         __syncthreads();
 
+        unsigned long long p_tw0 = 0;
         // ======== phase 1: evaluate + expand ========
         // staging items: short [0, n0c), long [n0c, n0c+n1c), hub [n0c+n1c, nwork)
         {
             RoundCtx RH{W2, n0c + n1c, FR, CE, fm_cur, scan_mode};
+            unsigned long long tw1 = 0, tw2 = 0, tw3 = 0;
+            const bool prof = ctl->prof != nullptr && lane == 0;
+            if (prof) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(p_tw0));
+            const unsigned long long tw0 = p_tw0;
             if (n2c > 0) {
                 for (;;) {  // hub rows: whole CTA per row (critical path first)
                     if (tid == 0) s_i[2] = (int)atomicAdd(&slot->grab[2], 1u);
@@ -1092,9 +1143,20 @@ __global__ void __launch_bounds__(kLpThreads, DLP_LP_MINB) k_lp_fused(LPParams P
             }
             (void)T;
 #else
-            warp_tiles(P, RL, K, B, T, sw, sx, sfu, &slot->grab[1], n1c, 1, pol);  // long rows: one per tile
-            warp_tiles(P, RS, K, B, T, sw, sx, sfu, &slot->grab[0], n0c, rpw, pol);  // short rows
+            if (prof) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tw1));
+#ifndef DLP_LONG_PER
+#define DLP_LONG_PER 1
 #endif
+            warp_tiles(P, RL, K, B, T, sw, sx, sfu, &slot->grab[1], n1c, DLP_LONG_PER, pol);  // long rows
+            if (prof) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tw2));
+            warp_tiles(P, RS, K, B, T, sw, sx, sfu, &slot->grab[0], n0c, rpw, pol);  // short rows
+            if (prof) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tw3));
+#endif
+            if (prof) {  // warp-time per part of phase 1 (diagnostics)
+                atomicAdd(&ctl->prof[0], tw1 - tw0);
+                atomicAdd(&ctl->prof[1], tw2 - tw1);
+                atomicAdd(&ctl->prof[2], tw3 - tw2);
+            }
         }
         if (K.claimed) atomicOr(&B.claimed, K.claimed);
         __syncthreads();
@@ -1111,6 +1173,11 @@ __global__ void __launch_bounds__(kLpThreads, DLP_LP_MINB) k_lp_fused(LPParams P
         }
         grid_sync(&ctl->bar, target);
         if (ctl->trace && gtid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_p1));
+        if (ctl->prof && (tid & 31) == 0) {
+            unsigned long long tnow;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));
+            atomicAdd(&ctl->prof[3], tnow - p_tw0);  // warp-ns from phase-1 start to the grid barrier's exit
+        }
 
         // ======== phase 2: commit (Jacobi), clear this round's masks ========
         // two items per thread in flight; full column masks move as 16-byte
@@ -1232,6 +1299,7 @@ __global__ void __launch_bounds__(kLpThreads, DLP_LP_MINB) k_lp_fused(LPParams P
             if (blockIdx.x == 0 && tid == 128) {
                 ctl->urows += (long long)vs->urows;
                 ctl->uentries += (long long)vs->uentries;
+                if (ctl->trace && R < ctl->trace_cap) ctl->trace[8 * R + 6] = vs->uentries;
             }
             __syncthreads();
             if (tid == 0) {
@@ -1368,6 +1436,10 @@ void lp_run_dev(Engine& E, double delta, long long max_iter, bool itlp) {
         DLP_CUDA_TRY(cudaMemsetAsync(E.lp_seen.p, 0, (E.cap_n + 1) * sizeof(int), E.st));
         int* sp = E.lp_seen.p;
         DLP_CUDA_TRY(cudaMemcpyAsync(&E.ctl->seen, &sp, sizeof(sp), cudaMemcpyHostToDevice, E.st));
+        E.lp_prof.reserve(8, 0, E.st);
+        DLP_CUDA_TRY(cudaMemsetAsync(E.lp_prof.p, 0, 8 * sizeof(unsigned long long), E.st));
+        unsigned long long* pp = E.lp_prof.p;
+        DLP_CUDA_TRY(cudaMemcpyAsync(&E.ctl->prof, &pp, sizeof(pp), cudaMemcpyHostToDevice, E.st));
         DLP_CUDA_TRY(cudaStreamSynchronize(E.st));  // host values above are stack temporaries
     }
     void* args[] = {&P};
@@ -1432,10 +1504,13 @@ void lp_dump_trace(Engine& E, long long rounds) {
     DLP_CUDA_TRY(cudaMemcpy(h.data(), E.lp_trace.p, h.size() * 8, cudaMemcpyDeviceToHost));
     FILE* fp = fopen(E.lp_trace_path, "a");
     if (!fp) return;
-    fprintf(fp, "# launch rounds=%lld grid=%d dups=%llu\n", rounds, E.lp_grid, E.h_ctl.p->dups);
+    unsigned long long pr[8] = {0};
+    DLP_CUDA_TRY(cudaMemcpy(pr, E.lp_prof.p, sizeof(pr), cudaMemcpyDeviceToHost));
+    fprintf(fp, "# launch rounds=%lld grid=%d dups=%llu prof_ms(warp-sum) hub=%.1f long=%.1f short=%.1f phase1=%.1f\n",
+            rounds, E.lp_grid, E.h_ctl.p->dups, pr[0] / 1e6, pr[1] / 1e6, pr[2] / 1e6, pr[3] / 1e6);
     for (long long r = 0; r < n; r++)
-        fprintf(fp, "%lld %llu %llu %llx %llu %llu %llu\n", r, h[8 * r], h[8 * r + 1], h[8 * r + 2], h[8 * r + 3],
-                h[8 * r + 4], h[8 * r + 5]);
+        fprintf(fp, "%lld %llu %llu %llx %llu %llu %llu %llu\n", r, h[8 * r], h[8 * r + 1], h[8 * r + 2],
+                h[8 * r + 3], h[8 * r + 4], h[8 * r + 5], h[8 * r + 6]);
     fclose(fp);
 }
 

@@ -16,7 +16,8 @@ def launches(path):
         f = ln.split()
         r, ns, nl, m, t = f[:5]
         p1, r0 = (int(f[5]), int(f[6])) if len(f) >= 7 else (0, 0)
-        cur.append((int(r), int(ns), int(nl), int(m, 16), int(t), p1, r0))
+        ue = int(f[7]) if len(f) >= 8 else 0
+        cur.append((int(r), int(ns), int(nl), int(m, 16), int(t), p1, r0, ue))
     if cur:
         out.append(np.array(cur, dtype=np.float64))
     return out
@@ -47,6 +48,14 @@ def summarise(a):
             if sel.any():
                 print(f"    rows [{lo:.0e},{hi:.0e}): phase1 {ph1[sel].mean():.1f} us, commit+controller "
                       f"{rest[sel].mean():.1f} us, inter-round {gap[sel].mean():.1f} us")
+    if a.shape[1] >= 8 and a[:, 7].sum() > 0:
+        ph1 = (a[:, 5] - a[:, 6]) / 1e3
+        ent = a[:, 7]
+        for lo, hi in [(0, 1e4), (1e4, 1e5), (1e5, 1e6), (1e6, 1e7), (1e7, 1e9)]:
+            sel = (ent >= lo) & (ent < hi)
+            if sel.any():
+                print(f"    entries [{lo:.0e},{hi:.0e}): rounds {sel.sum()}, phase1 total {ph1[sel].sum() / 1e3:.2f} ms, "
+                      f"{ent[sel].sum() / max(ph1[sel].sum(), 1e-9) / 1e3:.2f} G entries/s")
     if ce.any():
         print(f"  certify: us/round={dt[ce].mean():.1f} rows/round={rows[ce].mean():.0f} "
               f"long/round={nlong[ce].mean():.0f} hub/round={nhub[ce].mean():.0f}")
