@@ -442,8 +442,12 @@ def main():
     barrier()
     ev0.record()
     repsB = []
-    for b in batches[t0:]:
-        labB, r = step(gB, labB, b)
+    tb = batches[t0:]
+    for i, b in enumerate(tb):
+        if sharded:
+            labB, r = step(gB, labB, b)
+        else:  # ingestion pipeline: batch i+1 is validated and copied while batch i runs
+            labB, r = apply_batch(gB, labB, b, ecfg, next_batch=tb[i + 1] if i + 1 < len(tb) else None)
         repsB.append(r if isinstance(r, list) else [r])
         d2h = ctypes_report_bytes(ncol)
     ev1.record()

@@ -95,6 +95,13 @@ int dlp_num_columns(dlp_engine* e);
  * fixed at dlp_create (at most 16 label columns). */
 int dlp_apply_batch(dlp_engine* e, const dlp_config* cfg, const dlp_batch* batch,
                     dlp_report* reports);
+/* Ingestion pipeline: apply `batch` (HOST arrays) and, while
+ * its kernels run, validate `next` against the post-`batch` host mirror and
+ * copy it to the device on a copy stream.  The next call with the same
+ * `next` pointers skips its validation and copy (a validation error found
+ * early is returned by that call, before any mutation).  next may be NULL. */
+int dlp_apply_batch_pipelined(dlp_engine* e, const dlp_config* cfg, const dlp_batch* batch, const dlp_batch* next,
+                              dlp_report* reports);
 /* Same, batch arrays already resident in device memory (bench "value" leg).
  * Validation still runs against the engine's host mirror, so the arrays are
  * also read back for it unless `trusted` is nonzero. */

@@ -54,6 +54,7 @@ SIGNATURES = {
     "dlp_num_columns": (_int, [_p]),
     "dlp_apply_batch": (_int, [_p, _p, _p, _p]),
     "dlp_apply_batch_device": (_int, [_p, _p, _p, _int, _p]),
+    "dlp_apply_batch_pipelined": (_int, [_p, _p, _p, _p, _p]),
     "dlp_apply_structure": (_int, [_p, _p]),
     "dlp_itlp_batch": (_int, [_p, _p, _p, _p]),
     "dlp_reserve": (_int, [_p, _i64, _i64]),

@@ -152,8 +152,13 @@ __global__ void k_reset_batch(DevState* ds) {
 
 size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
-// Stage host batch arrays into one pinned buffer and copy it to the device.
-BatchDev stage_batch(Engine& E, const HostBatch& b) {
+// Stage host batch arrays into one pinned buffer and copy it to the device
+// (slot 0: the current batch on the compute stream; slot 1: the next batch
+// of the ingestion pipeline on the copy stream).
+BatchDev stage_batch(Engine& E, const HostBatch& b, int slot = 0, cudaStream_t st = nullptr) {
+    PinnedArray<unsigned char>& hs = slot ? E.h_stage2 : E.h_stage;
+    DevArray<unsigned char>& ds = slot ? E.d_stage2 : E.d_stage;
+    if (!st) st = E.st;
     size_t off[7];
     size_t sz[6] = {(size_t)b.k * 8, (size_t)b.k, (size_t)b.ne * 8, (size_t)b.ne * 8, (size_t)b.ne * 8, (size_t)b.nd * 8};
     size_t tot = 0;
@@ -162,12 +167,34 @@ BatchDev stage_batch(Engine& E, const HostBatch& b) {
         tot += align_up(sz[i]);
     }
     off[6] = tot;
-    E.h_stage.reserve(tot + 256);
-    E.d_stage.reserve(tot + 256, 0, E.st);
+    hs.reserve(tot + 256);
+    ds.reserve(tot + 256, 0, st);
     const void* src[6] = {b.ids, b.gt, b.owner, b.other, b.w, b.dels};
     for (int i = 0; i < 6; i++)
-        if (sz[i]) memcpy(E.h_stage.p + off[i], src[i], sz[i]);
-    if (tot) DLP_CUDA_TRY(cudaMemcpyAsync(E.d_stage.p, E.h_stage.p, tot, cudaMemcpyHostToDevice, E.st));
+        if (sz[i]) memcpy(hs.p + off[i], src[i], sz[i]);
+    if (tot) DLP_CUDA_TRY(cudaMemcpyAsync(ds.p, hs.p, tot, cudaMemcpyHostToDevice, st));
+    unsigned char* d = ds.p;
+    BatchDev bd;
+    bd.ids = (const long long*)(d + off[0]);
+    bd.gt = (const signed char*)(d + off[1]);
+    bd.owner = (const long long*)(d + off[2]);
+    bd.other = (const long long*)(d + off[3]);
+    bd.w = (const double*)(d + off[4]);
+    bd.dels = (const long long*)(d + off[5]);
+    bd.k = b.k;
+    bd.ne = b.ne;
+    bd.nd = b.nd;
+    return bd;
+}
+
+// device views of a batch already resident in the current staging slot
+BatchDev stage_view(Engine& E, const HostBatch& b) {
+    size_t sz[6] = {(size_t)b.k * 8, (size_t)b.k, (size_t)b.ne * 8, (size_t)b.ne * 8, (size_t)b.ne * 8, (size_t)b.nd * 8};
+    size_t off[6], tot = 0;
+    for (int i = 0; i < 6; i++) {
+        off[i] = tot;
+        tot += align_up(sz[i]);
+    }
     unsigned char* d = E.d_stage.p;
     BatchDev bd;
     bd.ids = (const long long*)(d + off[0]);
@@ -180,6 +207,47 @@ BatchDev stage_batch(Engine& E, const HostBatch& b) {
     bd.ne = b.ne;
     bd.nd = b.nd;
     return bd;
+}
+
+bool staged_matches(const Engine& E, const dlp_batch* b) {
+    const Engine::Staged& s = E.staged;
+    const void* p[6] = {b->insert_ids, b->insert_gt, b->edge_owner, b->edge_other, b->edge_w, b->deletes};
+    if (!s.valid || s.t != b->t || s.k != b->n_ins || s.ne != b->n_edges || s.nd != b->n_del) return false;
+    for (int i = 0; i < 6; i++)
+        if (s.ptrs[i] != p[i]) return false;
+    return true;
+}
+
+int validate_batch(Engine& E, const HostBatch& b);
+
+// Ingestion pipeline: validate the next batch against the
+// host mirror (already advanced past the current batch) and copy it to the
+// device on the copy stream while the current batch's kernels run.
+void stage_next(Engine& E, const dlp_batch* nb) {
+    Engine::Staged& s = E.staged;
+    s.valid = true;
+    s.t = nb->t;
+    s.k = nb->n_ins;
+    s.ne = nb->n_edges;
+    s.nd = nb->n_del;
+    const void* p[6] = {nb->insert_ids, nb->insert_gt, nb->edge_owner, nb->edge_other, nb->edge_w, nb->deletes};
+    for (int i = 0; i < 6; i++) s.ptrs[i] = p[i];
+    HostBatch hb{nb->t, nb->n_ins, nb->n_edges, nb->n_del, (const long long*)nb->insert_ids,
+                 (const long long*)nb->edge_owner, (const long long*)nb->edge_other, (const long long*)nb->deletes,
+                 (const signed char*)nb->insert_gt, nb->edge_w};
+    std::string saved = E.err;
+    s.rc = validate_batch(E, hb);
+    s.err = E.err;
+    E.err = saved;
+    if (s.rc) return;  // reported when the batch is applied; nothing staged
+    if (!E.cst) {
+        DLP_CUDA_TRY(cudaStreamCreateWithFlags(&E.cst, cudaStreamNonBlocking));
+        DLP_CUDA_TRY(cudaEventCreateWithFlags(&E.cev, cudaEventDisableTiming));
+    } else {
+        DLP_CUDA_TRY(cudaEventSynchronize(E.cev));  // an earlier staged copy may still read h_stage2
+    }
+    stage_batch(E, hb, 1, E.cst);
+    DLP_CUDA_TRY(cudaEventRecord(E.cev, E.cst));
 }
 
 enum Kind { KIND_DYNLP = 0, KIND_STRUCTURE = 1, KIND_ITLP = 2 };
@@ -319,7 +387,8 @@ int sharded_lp(Engine& E, const dlp_config* cfg, long long max_iter, dlp_allredu
 }
 
 int run_batch(dlp_engine* h, const dlp_config* cfg, const dlp_batch* batch, bool device_ptrs, bool trusted,
-              dlp_report* reps, Kind kind, dlp_allreduce_fn reduce = nullptr, void* rctx = nullptr) {
+              dlp_report* reps, Kind kind, dlp_allreduce_fn reduce = nullptr, void* rctx = nullptr,
+              const dlp_batch* next = nullptr) {
     Engine& E = h->E;
     auto t0 = std::chrono::steady_clock::now();
     if (h->poisoned) return fail(E, DLP_EINTERNAL, "engine is unusable after an earlier CUDA error");
@@ -378,7 +447,12 @@ int run_batch(dlp_engine* h, const dlp_config* cfg, const dlp_batch* batch, bool
             hb.w = hv_w.data();
             hb.dels = hv_dels.data();
         }
-        if (!(device_ptrs && trusted)) {
+        const bool use_staged = !device_ptrs && staged_matches(E, batch);
+        if (use_staged) {  // validated and copied during the previous batch
+            E.staged.valid = false;
+            if (E.staged.rc) return fail(E, E.staged.rc, "%s", E.staged.err.c_str());
+        } else if (!(device_ptrs && trusted)) {
+            E.staged.valid = false;
             int rc = validate_batch(E, hb);
             if (rc) return rc;
         }
@@ -401,6 +475,11 @@ int run_batch(dlp_engine* h, const dlp_config* cfg, const dlp_batch* batch, bool
             bd.k = k;
             bd.ne = ne;
             bd.nd = nd;
+        } else if (use_staged) {
+            std::swap(E.h_stage, E.h_stage2);  // the staged slot becomes the current one
+            std::swap(E.d_stage, E.d_stage2);
+            bd = stage_view(E, hb);
+            DLP_CUDA_TRY(cudaStreamWaitEvent(E.st, E.cev, 0));
         } else {
             bd = stage_batch(E, hb);
         }
@@ -482,6 +561,7 @@ int run_batch(dlp_engine* h, const dlp_config* cfg, const dlp_batch* batch, bool
         }
         DLP_CUDA_TRY(cudaGetLastError());
         host_mark(E, "enqueued");
+        if (next && !device_ptrs) stage_next(E, next);  // overlaps the kernels enqueued above
         DLP_CUDA_TRY(cudaMemcpyAsync(E.h_ds.p, E.ds, sizeof(DevState), cudaMemcpyDeviceToHost, E.st));
         DLP_CUDA_TRY(cudaMemcpyAsync(E.h_ctl.p, E.ctl, sizeof(LPCtl), cudaMemcpyDeviceToHost, E.st));
         DLP_CUDA_TRY(cudaStreamSynchronize(E.st));
@@ -578,6 +658,12 @@ int dlp_create(const dlp_config* cfg, int device, dlp_engine** out) {
     return DLP_OK;
 }
 
+int dlp_apply_batch_pipelined(dlp_engine* h, const dlp_config* cfg, const dlp_batch* batch, const dlp_batch* next,
+                              dlp_report* reports) {
+    if (!h) return DLP_EINTERNAL;
+    return run_batch(h, cfg, batch, false, false, reports, KIND_DYNLP, nullptr, nullptr, next);
+}
+
 int dlp_shard_set(dlp_engine* h, int rank, int world) {
     if (!h) return DLP_EINTERNAL;
     Engine& E = h->E;
@@ -660,6 +746,10 @@ int dlp_destroy(dlp_engine* h) {
     if (E.ds) cudaFree(E.ds);
     if (E.ctl) cudaFree(E.ctl);
     E.h_stage.release();
+    E.h_stage2.release();
+    E.d_stage2.release();
+    if (E.cev) cudaEventDestroy(E.cev);
+    if (E.cst) cudaStreamDestroy(E.cst);
     E.h_ds.release();
     E.h_ctl.release();
     for (auto ev : E.lp_ev)

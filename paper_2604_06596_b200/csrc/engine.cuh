@@ -194,8 +194,18 @@ struct Engine {
     DevArray<int> log_lo, log_hi, log_lo2, log_hi2;
     DevArray<double> log_w, log_w2;
     // batch staging -------------------------------------------------------
-    PinnedArray<unsigned char> h_stage;
-    DevArray<unsigned char> d_stage;
+    PinnedArray<unsigned char> h_stage, h_stage2;  // batch staging (two slots: ingestion pipeline)
+    DevArray<unsigned char> d_stage, d_stage2;
+    cudaStream_t cst = nullptr;   // copy stream of the ingestion pipeline
+    cudaEvent_t cev = nullptr;    // staged copy complete
+    struct Staged {               // next batch validated and copied during the previous batch
+        bool valid = false;
+        int rc = 0;
+        std::string err;
+        long long t = 0, k = 0, ne = 0, nd = 0;
+        const void* ptrs[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+        std::vector<long long> dels;  // host copy: mirror update when the batch is applied
+    } staged;
     // per-batch scratch -----------------------------------------------------
     DevArray<unsigned long long> key_a, key_b;
     DevArray<int> val_a, val_b, flag_i, pos_i;

@@ -265,8 +265,8 @@ class DynamicGraph:
             _raise(self._lib, self._h, rc)
 
     # -- batch application ------------------------------------------------------------
-    def _run(self, fn_name, batch, cfg: Optional[EngineConfig]):
-        t, ids, gt, owner, other, w, dels = as_arrays(batch)
+    def _run_arrays(self, fn_name, arrays, cfg: Optional[EngineConfig]):
+        t, ids, gt, owner, other, w, dels = arrays
         b = _native.Batch(t, len(ids), _native.ptr(ids), _native.ptr(gt), len(owner),
                           _native.ptr(owner), _native.ptr(other), _native.ptr(w), len(dels),
                           _native.ptr(dels))
@@ -282,6 +282,33 @@ class DynamicGraph:
         if rc != 0:
             _raise(self._lib, self._h, rc)
         return reps
+
+    def _run_pipelined(self, batch, next_batch, cfg: EngineConfig):
+        # the arrays of both batches must outlive the call; keep the staged
+        # batch's arrays referenced until the next call consumes them
+        cur = as_arrays(batch) if getattr(self, "_staged_src", (None,))[0] is not batch else self._staged_arrays
+        nxt = as_arrays(next_batch)
+        t, ids, gt, owner, other, w, dels = cur
+        b = _native.Batch(t, len(ids), _native.ptr(ids), _native.ptr(gt), len(owner), _native.ptr(owner),
+                          _native.ptr(other), _native.ptr(w), len(dels), _native.ptr(dels))
+        t2, ids2, gt2, owner2, other2, w2, dels2 = nxt
+        b2 = _native.Batch(t2, len(ids2), _native.ptr(ids2), _native.ptr(gt2), len(owner2), _native.ptr(owner2),
+                           _native.ptr(other2), _native.ptr(w2), len(dels2), _native.ptr(dels2))
+        reps = (_native.Report * self.ncol)()
+        c = cfg._c(self.num_classes)
+        rc = self._lib.dlp_apply_batch_pipelined(self._h, C.byref(c), C.byref(b), C.byref(b2), reps)
+        self._staged_src, self._staged_arrays = (next_batch,), nxt
+        self._version += 1
+        if rc != 0:
+            _raise(self._lib, self._h, rc)
+        return reps
+
+    def _run(self, fn_name, batch, cfg: Optional[EngineConfig]):
+        if getattr(self, "_staged_src", (None,))[0] is batch:
+            batch_arrays = self._staged_arrays  # same buffers the engine staged
+            self._staged_src = (None,)
+            return self._run_arrays(fn_name, batch_arrays, cfg)
+        return self._run_arrays(fn_name, as_arrays(batch), cfg)
 
     def apply_device(self, dev_batch: dict, cfg: EngineConfig, trusted: bool = True):
         """apply_batch with batch arrays already in device memory (torch
@@ -380,12 +407,20 @@ def _result(graph, reports):
     return reports[0] if graph.ncol == 1 else reports
 
 
-def apply_batch(graph: DynamicGraph, labels: LabelState, batch, cfg: EngineConfig):
+def apply_batch(graph: DynamicGraph, labels: LabelState, batch, cfg: EngineConfig, next_batch=None):
     """engine.apply_batch: returns (labels, IterationReport) for binary runs,
-    (labels, [IterationReport per class column]) for C > 2."""
+    (labels, [IterationReport per class column]) for C > 2.
+
+    ``next_batch`` (optional, B200 ingestion pipeline): the batch the caller
+    will apply next; it is validated and copied to the device while this
+    batch's kernels run, and the next call with the same object skips both
+    steps.  Results are identical either way."""
     cfg.validate()
     labels._bind(graph)
-    reps = graph._run("dlp_apply_batch", batch, cfg)
+    if next_batch is None:
+        reps = graph._run("dlp_apply_batch", batch, cfg)
+    else:
+        reps = graph._run_pipelined(batch, next_batch, cfg)
     return labels, _result(graph, _reports(reps, "dynlp"))
 
 
@@ -394,8 +429,15 @@ def apply_batch_structure(graph: DynamicGraph, labels: LabelState, batch) -> Non
     graph._run("dlp_apply_structure", batch, None)
 
 
-def run_batches(graph: DynamicGraph, labels: LabelState, batches, cfg: EngineConfig):
-    return [apply_batch(graph, labels, b, cfg)[1] for b in batches]
+def run_batches(graph: DynamicGraph, labels: LabelState, batches, cfg: EngineConfig, pipelined: bool = True):
+    """engine.run_batches; with ``pipelined`` each batch's validation and
+    host-to-device copy overlap the previous batch's propagation."""
+    batches = list(batches)
+    out = []
+    for i, b in enumerate(batches):
+        nxt = batches[i + 1] if pipelined and i + 1 < len(batches) else None
+        out.append(apply_batch(graph, labels, b, cfg, next_batch=nxt)[1])
+    return out
 
 
 def itlp_batch_solve(graph: DynamicGraph, labels: LabelState, batch, cfg: EngineConfig):

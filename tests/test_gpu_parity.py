@@ -214,3 +214,35 @@ def test_row_class_paths(gpu_device, ncls, long_row, hub_row):
     r = subprocess.run([sys.executable, os.path.join(here, "_row_class_check.py"), str(ncls)], env=env,
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+def test_ingestion_pipeline_identical_and_atomic(gpu_device):
+    """apply_batch(..., next_batch=) validates and stages the next batch while
+    the current one runs: identical reports and labels; a bad next batch is
+    reported by its own call and leaves the engine unchanged."""
+    from paper_2604_06596_b200.engine import DynamicGraph, EngineConfig, LabelState, apply_batch, run_batches
+
+    bl = streams.make_blobs(3000, 16, 3, 2)
+    e = streams.knn_graph_exact(bl.x, 8)
+    gt = streams.stratified_seeds(bl.classes, 0.02, 2)
+    s = streams.phased_stream(3000, e, bl.classes, gt, 300, 2, 0.8, 0.02, 0.18, initial_gt=6)
+    cfg = EngineConfig(delta=1e-5)
+    g1, l1 = DynamicGraph(0, num_classes=3), LabelState()
+    r1 = run_batches(g1, l1, s.batches, cfg, pipelined=False)
+    g2, l2 = DynamicGraph(0, num_classes=3), LabelState()
+    r2 = run_batches(g2, l2, s.batches, cfg, pipelined=True)
+    for a, b in zip(r1, r2):
+        assert [(x.iterations, x.updates, x.max_change) for x in a] == [(x.iterations, x.updates, x.max_change) for x in b]
+    assert l1.F.tobytes() == l2.F.tobytes()
+    # a next batch that deletes an unknown vertex: the error comes from its own call
+    bad = BatchUpdate(t=99, insert_ids=np.empty(0, np.int64), insert_gt=np.empty(0, np.int8),
+                      edge_owner=np.empty(0, np.int64), edge_other=np.empty(0, np.int64),
+                      edge_w=np.empty(0), deletes=np.array([10 ** 9], np.int64))
+    g3, l3 = DynamicGraph(0, num_classes=3), LabelState()
+    apply_batch(g3, l3, s.batches[0], cfg, next_batch=bad)
+    F_before = l3.F.copy()
+    with pytest.raises(ValidationError):
+        apply_batch(g3, l3, bad, cfg)
+    assert l3.F.tobytes() == F_before.tobytes()
+    for g in (g1, g2, g3):
+        g.close()
