@@ -49,6 +49,12 @@ CONFIGS = {
     "c1": dict(n=10_000, dim=16, classes=3, k=10, seed_frac=0.01, batch=500,
                fractions=(0.99, 0.01, 0.0), seed=0, delta=1e-4,
                desc="C1: synthetic blobs 10k x 16-dim, 3 classes, kNN k=10, 1% seeds, batches of 500"),
+    # configs[3]: 10M x 64, k=16, 0.1% seeds (binary, one column), batches of 100k; the
+    # working set (labels 80 MB x ... adjacency ~2.4 GB) is far beyond L2
+    "c4": dict(n=10_000_000, dim=64, classes=2, k=16, seed_frac=0.001, batch=100_000,
+               fractions=(0.99, 0.01, 0.0), seed=1, delta=1e-4,
+               desc="C4: synthetic blobs 10M x 64-dim, binary, cosine kNN k=16, 0.1% seeds, "
+                    "insert batches of 100k (single GPU)"),
     # configs[2]: the C2 graph statistics with mixed 70/30 insert/delete batches
     "c3": dict(n=1_000_000, dim=128, classes=10, k=10, seed_frac=0.01, batch=10_000,
                fractions=(0.69, 0.01, 0.30), seed=0, delta=1e-4,
