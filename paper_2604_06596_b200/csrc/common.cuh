@@ -61,20 +61,6 @@ struct RowAcc {
             s = __dadd_rn(s, __dmul_rn(__dsub_rn(fv, fu), w));
     }
     // same, with x = the NaN-boxed label word of the neighbour.
-#ifdef DLP_BRANCHY_ACC
-    // ground-truth neighbours (~1% of entries) take a rarely-divergent branch
-    __device__ inline void add_boxed(double w, double x, double fu) {
-        w_all = __dadd_rn(w_all, w);
-        if (__builtin_expect(is_boxed(x), 0)) {
-            if (boxed_class(x) == 0)
-                w0 = __dadd_rn(w0, w);
-            else
-                w1 = __dadd_rn(w1, w);
-        } else {
-            s = __dadd_rn(s, __dmul_rn(__dsub_rn(x, fu), w));
-        }
-    }
-#else
     // Branch-free: the sums that do not take this entry add +0.0, which leaves
     // them bit-identical (they are never -0.0: they start at +0.0 and a sum
     // that cancels to zero rounds to +0.0), so the four chains pipeline.
@@ -87,7 +73,6 @@ struct RowAcc {
         w1 = __dadd_rn(w1, (gt && cls == 1) ? w : 0.0);
         s = __dadd_rn(s, gt ? 0.0 : p);
     }
-#endif
     // returns |fn - fu| or -1 for the isolated sentinel (value 0.5)
     __device__ inline double finish(double fu, double* out_val) const {
         if (w_all <= 0.0) {
@@ -132,12 +117,9 @@ __device__ inline void grid_sync(unsigned int* ctr, unsigned int& target) {
         target += gridDim.x;
         __threadfence();
         atomicAdd(ctr, 1u);
-#ifdef DLP_SPIN_SLEEP
-        while (ld_acquire_u32(ctr) < target) __nanosleep(DLP_SPIN_SLEEP);
-#else
         while (ld_acquire_u32(ctr) < target) {
         }
-#endif
+
         __threadfence();
     }
     __syncthreads();

@@ -65,6 +65,10 @@ constexpr int kLpThreads = 256;
 #define DLP_ACC_UNROLL 4
 #endif
 constexpr int kAccUnroll = DLP_ACC_UNROLL;  // ordered-sum loop unroll
+#ifndef DLP_EXPAND_REGS
+#define DLP_EXPAND_REGS 1
+#endif
+constexpr bool kExpandRegs = DLP_EXPAND_REGS;  // expand single-window tiles from the gather registers
 constexpr int kWin = DLP_WIN;   // row entries per warp window
 constexpr int kHubWin = DLP_HUB_WIN;  // row entries per CTA window (hub rows)
 constexpr int kLongRow = 96;    // rows longer than this are warp tiles of their own
@@ -154,16 +158,8 @@ __device__ inline void cp_async8(double* dst, const double* src, unsigned long l
 }
 __device__ inline void cp_async16(double* dst, const double* src, unsigned long long pol) {
     unsigned int d = (unsigned int)__cvta_generic_to_shared(dst);
-#ifdef DLP_CP_CA
-    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "l"(pol)
-                 : "memory");
-#elif defined(DLP_CP_NOHINT)
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
-    (void)pol;
-#else
     asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "l"(pol)
                  : "memory");
-#endif
 }
 __device__ inline void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
@@ -422,15 +418,8 @@ __device__ void warp_tile(const LPParams& P, const RoundCtx& R, ClaimCtx& K, Blo
             atomicAdd(&B.uent, (unsigned long long)total);
         }
     }
-#ifdef DLP_SYNC_FU
-    for (int i = lane; i < nrows * C; i += 32) {
-        int r = i / C, c = i - r * C;
-        sfu[i] = ((T.em[r] >> c) & 1u) ? P.X[(long long)T.u[r] * C + c] : 0.0;
-    }
-#else
     // own label rows ride with the first window's asynchronous copies
     if (lane < nrows && T.em[lane]) copy_label_row(sfu + lane * C, P.X + (long long)T.u[lane] * C, C, pol);
-#endif
     *mn = load_meta(P, R, un);  // next tile's metadata, consumed next iteration
     __syncwarp();
     // ---- accumulate lanes
@@ -477,37 +466,8 @@ __device__ void warp_tile(const LPParams& P, const RoundCtx& R, ClaimCtx& K, Blo
         if (aact) {
             const double fu = sfu[ar * C + ac];
             const int lo = max(a_lo, wb) - wb, hi = min(a_hi, wb + wn) - wb;
-#ifdef DLP_GT_SPLIT
-            // The four sums are independent chains: w_all and s over the window
-            // here (a ground-truth entry adds (fu - fu) * w = +0.0 to s, which is
-            // bit-neutral), w0 / w1 only over the rare ground-truth entries in a
-            // second ordered pass -- each chain still sees its entries in row order.
-            bool any_gt = false;
-            double s_ = acc.s, wa = acc.w_all;
-#pragma unroll kAccUnroll
-            for (int t = lo; t < hi; t++) {
-                const double w = sw[t], x = sx[t * C + ac];
-                const bool g = is_boxed(x);
-                any_gt |= g;
-                wa = __dadd_rn(wa, w);
-                s_ = __dadd_rn(s_, __dmul_rn(__dsub_rn(g ? fu : x, fu), w));
-            }
-            acc.s = s_;
-            acc.w_all = wa;
-            if (any_gt) {
-                for (int t = lo; t < hi; t++) {
-                    const double x = sx[t * C + ac];
-                    if (!is_boxed(x)) continue;
-                    if (boxed_class(x) == 0)
-                        acc.w0 = __dadd_rn(acc.w0, sw[t]);
-                    else
-                        acc.w1 = __dadd_rn(acc.w1, sw[t]);
-                }
-            }
-#else
 #pragma unroll kAccUnroll
             for (int t = lo; t < hi; t++) acc.add_boxed(sw[t], sx[t * C + ac], fu);
-#endif
         }
         __syncwarp();
     }
@@ -550,7 +510,7 @@ __device__ void warp_tile(const LPParams& P, const RoundCtx& R, ClaimCtx& K, Blo
                 claim(K, T.u[lane], m);
         }
     }
-    if (total <= kWin) {
+    if (kExpandRegs && total <= kWin) {
         // single-window tile: the gathering lanes still hold the entries' ids
 #pragma unroll
         for (int j = 0; j < kWin / 32; j++) {
@@ -1118,7 +1078,11 @@ __global__ void __launch_bounds__(kLpThreads, DLP_LP_MINB) k_lp_fused(LPParams P
         {
             RoundCtx RH{W2, n0c + n1c, FR, CE, fm_cur, scan_mode};
             unsigned long long tw1 = 0, tw2 = 0, tw3 = 0;
+#ifdef DLP_PROF
             const bool prof = ctl->prof != nullptr && lane == 0;
+#else
+            constexpr bool prof = false;  // build with -DDLP_PROF for the phase-1 warp-time profile
+#endif
             if (prof) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(p_tw0));
             const unsigned long long tw0 = p_tw0;
             if (n2c > 0) {
@@ -1173,11 +1137,13 @@ __global__ void __launch_bounds__(kLpThreads, DLP_LP_MINB) k_lp_fused(LPParams P
         }
         grid_sync(&ctl->bar, target);
         if (ctl->trace && gtid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_p1));
+#ifdef DLP_PROF
         if (ctl->prof && (tid & 31) == 0) {
             unsigned long long tnow;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));
             atomicAdd(&ctl->prof[3], tnow - p_tw0);  // warp-ns from phase-1 start to the grid barrier's exit
         }
+#endif
 
         // ======== phase 2: commit (Jacobi), clear this round's masks ========
         // two items per thread in flight; full column masks move as 16-byte
