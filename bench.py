@@ -477,7 +477,7 @@ def main():
     achieved = alg_bytes / (lp_ms * 1e-3) / 1e9 if lp_ms > 0 and uent > 0 else None
     survey_bytes = 32.0 * upd + 21.0 * edges  # SURVEY §8(d) D-4 per-column model
     peak, peak_kind = measured_peaks()
-    tr = traffic_record()
+    tr = traffic_record() if args.config == "c2" and not args.n else None  # the capture is of C2
     same = all(a[c].iterations == b[c].iterations and a[c].updates == b[c].updates
                for a, b in zip(repsA, repsB) for c in range(len(a)))
     line = {
