@@ -189,6 +189,10 @@ struct ClaimCtx {
     const unsigned int* eligm;
     const int* row_len;
     unsigned int claimed;  // per-thread OR of claimed column bits
+    // per-lane round counters of the lane's label column (flushed once per round)
+    unsigned long long c_nev, c_edg;
+    unsigned int c_warn;
+    double c_rmax;
 };
 
 // append-mode claim: add v (for the columns in `bits` where it is eligible)
@@ -483,14 +487,14 @@ __device__ void warp_tile(const LPParams& P, const RoundCtx& R, ClaimCtx& K, Blo
         double val;
         double d = acc.finish(fu, &val);
         __stcs(P.Y + (R.ybase + k0 + ar) * C + ac, val);
-        atomicAdd(&B.neval[ac], 1ULL);
-        atomicAdd(&B.edges[ac], (unsigned long long)T.len[ar]);
+        K.c_nev++;
+        K.c_edg += (unsigned long long)T.len[ar];
         if (d < 0.0) {  // isolated sentinel (_csr.pyx:49-51, 170-173)
-            atomicAdd(&B.warn[ac], 1ULL);
+            K.c_warn++;
             atomicAnd(&P.eligm[u], ~(1u << ac));
             atomicAdd((unsigned long long*)&P.ctl->elig_count[ac], ~0ULL);
         } else {
-            if (d > 0.0) atomicMax(&B.rmax[ac], dbits(d));
+            K.c_rmax = fmax(K.c_rmax, d);
             if (!P.itlp && d > P.delta) ch = 1u << ac;
         }
     }
@@ -786,14 +790,14 @@ __device__ void pc_consume(const LPParams& P, bool scan_mode, ClaimCtx& K, Block
                 double val;
                 double d = acc.finish(fu, &val);
                 __stcs(P.Y + (*S.ybase + ar) * C + ac, val);
-                atomicAdd(&B.neval[ac], 1ULL);
-                atomicAdd(&B.edges[ac], (unsigned long long)S.len[ar]);
+                K.c_nev++;
+                K.c_edg += (unsigned long long)S.len[ar];
                 if (d < 0.0) {  // isolated sentinel (_csr.pyx:49-51, 170-173)
-                    atomicAdd(&B.warn[ac], 1ULL);
+                    K.c_warn++;
                     atomicAnd(&P.eligm[u], ~(1u << ac));
                     atomicAdd((unsigned long long*)&P.ctl->elig_count[ac], ~0ULL);
                 } else {
-                    if (d > 0.0) atomicMax(&B.rmax[ac], dbits(d));
+                    K.c_rmax = fmax(K.c_rmax, d);
                     if (!P.itlp && d > P.delta) ch = 1u << ac;
                 }
             }
@@ -1058,7 +1062,8 @@ __global__ void __launch_bounds__(kLpThreads, DLP_LP_MINB) k_lp_fused(LPParams P
         const bool scan_mode = !P.itlp && nwork * kScanRatio >= n;
         unsigned int* fm_cur = P.fmask[ri];
         unsigned int* fm_next = P.fmask[rn];
-        ClaimCtx K{fm_next, {P.flist[0][rn], P.flist[1][rn], P.flist[2][rn]}, slot->cnt, P.eligm, P.row_len, 0u};
+        ClaimCtx K{fm_next, {P.flist[0][rn], P.flist[1][rn], P.flist[2][rn]}, slot->cnt, P.eligm, P.row_len, 0u,
+                   0ULL, 0ULL, 0u, 0.0};
         if (tid < kMaxCols) {
             B.rmax[tid] = 0;
             B.neval[tid] = 0;
@@ -1123,6 +1128,13 @@ __global__ void __launch_bounds__(kLpThreads, DLP_LP_MINB) k_lp_fused(LPParams P
             }
         }
         if (K.claimed) atomicOr(&B.claimed, K.claimed);
+        if (K.c_nev) {  // lane (row, c) tiles always give this lane column c
+            const int col = lane % C;
+            atomicAdd(&B.neval[col], K.c_nev);
+            atomicAdd(&B.edges[col], K.c_edg);
+            if (K.c_warn) atomicAdd(&B.warn[col], (unsigned long long)K.c_warn);
+            if (K.c_rmax > 0.0) atomicMax(&B.rmax[col], dbits(K.c_rmax));
+        }
         __syncthreads();
         if (tid < C) {
             if (B.rmax[tid]) atomicMax(&slot->rmax[tid], B.rmax[tid]);
