@@ -292,6 +292,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-knn", action="store_true", help="skip the k-NN edge-construction leg")
     ap.add_argument("--replicas", action="store_true", help="N > 1: independent replicas instead of sharding")
+    ap.add_argument("--no-itlp", action="store_true", help="skip the ItLP comparison leg")
     ap.add_argument("--cpu-kind", default=None, choices=[None, "reference", "port"])
     args = ap.parse_args()
 
@@ -489,8 +490,8 @@ def main():
                    "label_columns": ncol, "delta": delta,
                    "parallelism": (f"component-sharded x{world} (NCCL phase all-reduce)" if sharded
                                    else f"replicas x{world}"),
-                   "l2": "no flush: per-batch working set (adjacency ~200 MB + 10 label columns) exceeds "
-                         "the 126 MB L2"},
+                   "l2": "no flush: each batch's working set (adjacency pool, edge log, label and staging "
+                         "columns) exceeds the 126 MB L2"},
         "edges_per_s": edges / (ms_value * K * 1e-3),
         "vertex_updates_per_batch": upd / K, "edge_relaxations_per_batch": edges / K,
         "lp_kernel_share": lp_ms / (ms_value * K),
@@ -517,6 +518,22 @@ def main():
         "certify_sweeps_per_batch": sum(r.certify_sweeps for step in repsA for r in step) / K,
         "legs_identical_work": same,
     }
+    if rank == 0 and not args.no_itlp and not sharded:
+        # the paper's comparison: ItLP (full sweeps, baselines.py:236-253)
+        # on the same first timed batch from the same state, on the B200
+        from paper_2604_06596_b200.engine import itlp_batch_solve
+
+        gC, labC = bootstrap()
+        s_ = time.perf_counter()
+        _, repI = itlp_batch_solve(gC, labC, batches[t0], ecfg)
+        wall_itlp = (time.perf_counter() - s_) * 1e3
+        repI = repI if isinstance(repI, list) else [repI]
+        gC.close()
+        line["itlp"] = {"ms": wall_itlp, "lp_kernel_ms": repI[0].lp_kernel_ms,
+                        "sweeps_per_column": [r.iterations for r in repI],
+                        "updates": sum(r.updates for r in repI),
+                        "dynlp_ms_same_batch": repsA[0][0].wall_time_ms,
+                        "speedup_dynlp_vs_itlp": wall_itlp / max(repsA[0][0].wall_time_ms, 1e-9)}
     if rank == 0 and not args.no_knn:
         line["knn"] = knn_leg(cfg, batches, local, K)
     if rank == 0 and not args.no_cpu_baseline:

@@ -29,5 +29,8 @@ for r in range(5):
     rep = reps[0]
     res.append((rep.lp_kernel_ms, rep.lp_union_rows, rep.lp_union_entries, rep.iterations))
 best = min(res)
+tr = os.environ.get("DLP_LP_TRACE")
+if tr and os.path.exists(tr):
+    print([ln.strip() for ln in open(tr) if ln.startswith("#")][-1])
 print(f"sweep: {best[0]:.3f} ms, rows {best[1]}, entries {best[2]}, "
       f"{best[2] / best[0] / 1e6:.2f} G entries/s  all={[round(x[0], 3) for x in res]}")
