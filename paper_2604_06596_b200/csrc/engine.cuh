@@ -133,15 +133,19 @@ template <typename T>
 struct PinnedArray {
     T* p = nullptr;
     size_t n = 0;
+    std::vector<void*> retired;  // outgrown buffers, freed at release(): cudaFreeHost would
+                                 // synchronize the device in the middle of a batch
     void reserve(size_t want) {
         if (want <= n) return;
-        if (p) cudaFreeHost(p);
+        if (p) retired.push_back(p);
         size_t nn = want + want / 2 + 1024;
         DLP_CUDA_TRY(cudaMallocHost(&p, nn * sizeof(T)));
         n = nn;
     }
     void release() {
         if (p) cudaFreeHost(p);
+        for (void* q : retired) cudaFreeHost(q);
+        retired.clear();
         p = nullptr;
         n = 0;
     }
