@@ -288,10 +288,13 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
-    ap.add_argument("--n", type=int, default=None, help="override point count (smaller smoke runs)")
+    ap.add_argument("--points", "--n", dest="n", type=int, default=None,
+                    help="override point count (smaller smoke runs; --points under torchrun)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-knn", action="store_true", help="skip the k-NN edge-construction leg")
     ap.add_argument("--replicas", action="store_true", help="N > 1: independent replicas instead of sharding")
+    ap.add_argument("--shard-mode", default="components", choices=["components", "rows"],
+                    help="N > 1: shard connected components, or partition rows (giant component)")
     ap.add_argument("--no-itlp", action="store_true", help="skip the ItLP comparison leg")
     ap.add_argument("--cpu-kind", default=None, choices=[None, "reference", "port"])
     args = ap.parse_args()
@@ -353,7 +356,7 @@ def main():
 
     def new_graph():
         if sharded:
-            return ShardedGraph(local, max(2, cfg["classes"]), rank, world, coll), LabelState()
+            return ShardedGraph(local, max(2, cfg["classes"]), rank, world, coll, args.shard_mode), LabelState()
         return DynamicGraph(local, num_classes=max(2, cfg["classes"])), LabelState()
 
     def step(g, lab, b):
@@ -488,7 +491,9 @@ def main():
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": cfg["desc"], "points": cfg["n"], "timed_batches": f"t={t0}..{T - 1}",
                    "label_columns": ncol, "delta": delta,
-                   "parallelism": (f"component-sharded x{world} (NCCL phase all-reduce)" if sharded
+                   "parallelism": ((f"component-sharded x{world} (NCCL phase all-reduce)"
+                                    if args.shard_mode == "components" else
+                                    f"row-partitioned x{world} (per-round NCCL row all-gather)") if sharded
                                    else f"replicas x{world}"),
                    "l2": "no flush: each batch's working set (adjacency pool, edge log, label and staging "
                          "columns) exceeds the 126 MB L2"},

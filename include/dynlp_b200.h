@@ -132,6 +132,14 @@ int dlp_reserve(dlp_engine* e, int64_t n_vertices, int64_t n_edges);
 typedef int (*dlp_allreduce_fn)(void* ctx, int64_t* imax, int32_t nimax, int64_t* isum, int32_t nisum, double* dmax,
                                 int32_t ndmax);
 int dlp_shard_set(dlp_engine* e, int rank, int world);
+/* Row partition instead of component sharding (for a single giant component,
+ * SURVEY.md §8(e) E-3): rank r evaluates the rows v % world == r; after every
+ * global round the evaluated rows (vertex, masks, new labels) are all-gathered
+ * through the same callback (isum segments) and each rank applies the others'
+ * labels and frontier claims, so every rank holds the whole label matrix.
+ * Must be chosen before the first batch. */
+enum { DLP_SHARD_COMPONENTS = 0, DLP_SHARD_ROWS = 1 };
+int dlp_shard_mode(dlp_engine* e, int mode);
 int dlp_apply_batch_sharded(dlp_engine* e, const dlp_config* cfg, const dlp_batch* batch, dlp_allreduce_fn reduce,
                             void* ctx, dlp_report* reports);
 int dlp_read_owned(dlp_engine* e, uint8_t* owned, int64_t n);

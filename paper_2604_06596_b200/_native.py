@@ -59,6 +59,7 @@ SIGNATURES = {
     "dlp_itlp_batch": (_int, [_p, _p, _p, _p]),
     "dlp_reserve": (_int, [_p, _i64, _i64]),
     "dlp_shard_set": (_int, [_p, _int, _int]),
+    "dlp_shard_mode": (_int, [_p, _int]),
     "dlp_apply_batch_sharded": (_int, [_p, _p, _p, _p, _p, _p]),
     "dlp_read_owned": (_int, [_p, _p, _i64]),
     "dlp_num_slots": (_int, [_p, _p, _p]),

@@ -261,9 +261,87 @@ struct ColCtl {
     int act = ACT_NONE;
 };
 
+// Row partition: after each one-round launch, all-gather the round's
+// evaluated rows (vertex, evaluated mask, changed mask, new labels) through the
+// caller's sum-reduction (each rank fills its own segment; int64 sums of one
+// nonzero term are exact, labels travel as bit patterns), then apply the other
+// ranks' rows: labels, and the claims their changed rows make on this rank's
+// vertices.  Afterwards every rank holds the whole label matrix and its part
+// of the next global frontier; h_ctl->has_fr is refreshed.
+int rows_exchange(Engine& E, dlp_allreduce_fn reduce, void* rctx) {
+    const int C = E.ncol, W = E.shard_world, me = E.shard_rank;
+    LPCtl& L = *E.h_ctl.p;
+    const long long n = L.log_n;
+    std::vector<int> hu(n);
+    std::vector<unsigned int> hem(n), hchg(n);
+    std::vector<double> hy((size_t)n * C);
+    if (n) {
+        DLP_CUDA_TRY(cudaMemcpyAsync(hu.data(), E.log_u.p, n * 4, cudaMemcpyDeviceToHost, E.st));
+        DLP_CUDA_TRY(cudaMemcpyAsync(hem.data(), E.log_em.p, n * 4, cudaMemcpyDeviceToHost, E.st));
+        DLP_CUDA_TRY(cudaMemcpyAsync(hchg.data(), E.log_chg.p, n * 4, cudaMemcpyDeviceToHost, E.st));
+        DLP_CUDA_TRY(cudaMemcpyAsync(hy.data(), E.f[1].p, (size_t)n * C * 8, cudaMemcpyDeviceToHost, E.st));
+        DLP_CUDA_TRY(cudaMemsetAsync(E.log_chg.p, 0, n * 4, E.st));
+        DLP_CUDA_TRY(cudaStreamSynchronize(E.st));
+    }
+    std::vector<long long> keep;
+    for (long long i = 0; i < n; i++)
+        if (hem[i]) keep.push_back(i);
+    const int rec = 3 + C;
+    std::vector<int64_t> cnt(W, 0), z(1, 0);
+    std::vector<double> zd(1, 0.0);
+    cnt[me] = (int64_t)keep.size();
+    if (reduce(rctx, z.data(), 1, cnt.data(), W, zd.data(), 1)) return fail(E, DLP_EINTERNAL, "collective failed");
+    long long tot = 0, off = 0;
+    for (int r = 0; r < W; r++) {
+        if (r == me) off = tot;
+        tot += cnt[r];
+    }
+    if (tot == 0) return DLP_OK;
+    std::vector<int64_t> buf((size_t)tot * rec, 0);
+    for (size_t j = 0; j < keep.size(); j++) {
+        const long long i = keep[j];
+        int64_t* b = buf.data() + (size_t)(off + j) * rec;
+        b[0] = hu[i];
+        b[1] = hem[i];
+        b[2] = hchg[i];
+        memcpy(b + 3, hy.data() + (size_t)i * C, (size_t)C * 8);
+    }
+    if (buf.size() > (size_t)INT32_MAX) return fail(E, DLP_EINTERNAL, "row exchange too large");
+    if (reduce(rctx, z.data(), 1, buf.data(), (int32_t)buf.size(), zd.data(), 1))
+        return fail(E, DLP_EINTERNAL, "collective failed");
+    const long long m = tot - cnt[me];
+    if (m == 0) return DLP_OK;
+    std::vector<int> ru(m);
+    std::vector<unsigned int> rem(m), rchg(m);
+    std::vector<double> rv((size_t)m * C);
+    long long k = 0;
+    for (long long j = 0; j < tot; j++) {
+        if (j >= off && j < off + cnt[me]) continue;
+        const int64_t* b = buf.data() + (size_t)j * rec;
+        ru[k] = (int)b[0];
+        rem[k] = (unsigned int)b[1];
+        rchg[k] = (unsigned int)b[2];
+        memcpy(rv.data() + (size_t)k * C, b + 3, (size_t)C * 8);
+        k++;
+    }
+    E.rx_u.reserve(m, 0, E.st);
+    E.rx_em.reserve(m, 0, E.st);
+    E.rx_chg.reserve(m, 0, E.st);
+    E.rx_val.reserve((size_t)m * C, 0, E.st);
+    DLP_CUDA_TRY(cudaMemcpyAsync(E.rx_u.p, ru.data(), m * 4, cudaMemcpyHostToDevice, E.st));
+    DLP_CUDA_TRY(cudaMemcpyAsync(E.rx_em.p, rem.data(), m * 4, cudaMemcpyHostToDevice, E.st));
+    DLP_CUDA_TRY(cudaMemcpyAsync(E.rx_chg.p, rchg.data(), m * 4, cudaMemcpyHostToDevice, E.st));
+    DLP_CUDA_TRY(cudaMemcpyAsync(E.rx_val.p, rv.data(), (size_t)m * C * 8, cudaMemcpyHostToDevice, E.st));
+    lp_rows_apply(E, m, L.r_par);
+    DLP_CUDA_TRY(cudaMemcpyAsync(L.has_fr, E.ctl->has_fr, sizeof(L.has_fr), cudaMemcpyDeviceToHost, E.st));
+    DLP_CUDA_TRY(cudaStreamSynchronize(E.st));
+    return DLP_OK;
+}
+
 int sharded_lp(Engine& E, const dlp_config* cfg, long long max_iter, dlp_allreduce_fn reduce, void* rctx,
                std::vector<ColCtl>& col, double* lp_ms, long long* launches) {
     const int C = E.ncol;
+    const bool rows = E.shard_rows != 0;
     // global F0 emptiness and eligible counts (replicated structure, sharded sets)
     // label migration for components that changed owner (replicated order)
     {
@@ -329,6 +407,7 @@ int sharded_lp(Engine& E, const dlp_config* cfg, long long max_iter, dlp_allredu
         for (int c = 0; c < C; c++) {
             act[c] = col[c].act;
             budget[c] = max_iter - col[c].iterations;
+            if (rows) budget[c] = std::min(budget[c], 1LL);  // one global round per launch
         }
         DLP_CUDA_TRY(cudaMemcpyAsync(E.ctl->act, act, sizeof(act), cudaMemcpyHostToDevice, E.st));
         DLP_CUDA_TRY(cudaMemcpyAsync(E.ctl->budget, budget, sizeof(budget), cudaMemcpyHostToDevice, E.st));
@@ -336,6 +415,10 @@ int sharded_lp(Engine& E, const dlp_config* cfg, long long max_iter, dlp_allredu
         first = false;
         DLP_CUDA_TRY(cudaMemcpyAsync(E.h_ctl.p, E.ctl, sizeof(LPCtl), cudaMemcpyDeviceToHost, E.st));
         DLP_CUDA_TRY(cudaStreamSynchronize(E.st));
+        if (rows) {
+            int rc = rows_exchange(E, reduce, rctx);
+            if (rc) return rc;
+        }
         const LPCtl& L = *E.h_ctl.p;
         // reduce: max rounds | sum updates, edges, warnings, frontier, eligible | max rmax
         std::vector<int64_t> rmaxv(C), sums(5 * C);
@@ -673,6 +756,16 @@ int dlp_shard_set(dlp_engine* h, int rank, int world) {
     return DLP_OK;
 }
 
+int dlp_shard_mode(dlp_engine* h, int mode) {
+    if (!h) return DLP_EINTERNAL;
+    Engine& E = h->E;
+    if (mode != DLP_SHARD_COMPONENTS && mode != DLP_SHARD_ROWS) return fail(E, DLP_EVALIDATION, "bad shard mode");
+    if (E.n_slots != 0 && mode != E.shard_rows)
+        return fail(E, DLP_EVALIDATION, "the shard mode must be chosen before the first batch");
+    E.shard_rows = mode;
+    return DLP_OK;
+}
+
 int dlp_apply_batch_sharded(dlp_engine* h, const dlp_config* cfg, const dlp_batch* batch, dlp_allreduce_fn reduce,
                             void* ctx, dlp_report* reports) {
     if (!h) return DLP_EINTERNAL;
@@ -688,7 +781,8 @@ int dlp_read_owned(dlp_engine* h, uint8_t* owned, int64_t n) {
         DLP_CUDA_TRY(cudaSetDevice(E.device));
         std::vector<unsigned char> o(n);
         if (n) DLP_CUDA_TRY(cudaMemcpy(o.data(), E.owner_rank.p, n, cudaMemcpyDeviceToHost));
-        for (long long v = 0; v < n; v++) owned[v] = E.shard_world <= 1 || o[v] == E.shard_rank;
+        for (long long v = 0; v < n; v++)
+            owned[v] = E.shard_world <= 1 || (E.shard_rows ? v % E.shard_world == E.shard_rank : o[v] == E.shard_rank);
     } catch (const CudaFailure& f) {
         return cuda_fail(h, f);
     }
@@ -734,12 +828,13 @@ int dlp_destroy(dlp_engine* h) {
                              &E.ulist[0], &E.ulist[1], &E.llist[0], &E.llist[1], &E.hlist[0], &E.hlist[1], &E.elist_s, &E.elist_l, &E.elist_h, &E.f0, &E.elist, &E.purge_list, &E.touched,
                              &E.nbr, &E.nbr_sp, &E.log_lo, &E.log_hi, &E.log_lo2, &E.log_hi2, &E.val_a, &E.val_b,
                              &E.flag_i, &E.pos_i, &E.m_lo, &E.m_hi, &E.mlo_at, &E.mhi_at, &E.lpar, &E.comp,
-                             &E.comp_sorted_i, &E.root_flag, &E.root_rank, &E.root_tmp};
+                             &E.comp_sorted_i, &E.root_flag, &E.root_rank, &E.root_tmp, &E.log_u, &E.rx_u};
     for (auto* a : i32s) a->release();
     DevArray<double>* f64s[] = {&E.f[0], &E.f[1], &E.wgt, &E.wgt_sp, &E.log_w, &E.log_w2, &E.m_w, &E.ew_lo, &E.ew_hi,
-                                &E.mw_at, &E.per0, &E.per1, &E.cinit, &E.tau_scratch};
+                                &E.mw_at, &E.per0, &E.per1, &E.cinit, &E.tau_scratch, &E.rx_val};
     for (auto* a : f64s) a->release();
-    DevArray<unsigned int>* u32s[] = {&E.eligm, &E.emask_store, &E.fmask[0], &E.fmask[1]};
+    DevArray<unsigned int>* u32s[] = {&E.eligm, &E.emask_store, &E.fmask[0], &E.fmask[1], &E.log_em, &E.log_chg,
+                                      &E.rx_em, &E.rx_chg};
     for (auto* x : u32s) x->release();
     E.key_a.release();
     E.key_b.release();

@@ -101,6 +101,7 @@ struct LPCtl {
     long long r_par;               // rounds executed in this batch (list parity)
     unsigned int ncur_p[3];        // frontier list lengths at exit
     int started;                   // prologue done for this batch
+    long long log_n;               // row-partitioned mode: work items of the launch's round
 };
 enum { ACT_NONE = 0, ACT_FRONTIER = 1, ACT_CERTIFY = 2 };
 
@@ -178,6 +179,12 @@ struct Engine {
     long long intra_k = 0;
     bool cc_valid = true;  // global union-find consistent with the live graph
     int shard_rank = 0, shard_world = 1;  // component sharding (dlp_shard_set)
+    int shard_rows = 0;  // 1: row partition (dlp_shard_mode): vertex v is owned by rank v % world
+    // row partition: per-round work-item log (vertex, evaluated mask, changed
+    // mask; the values are the compact staging Y) and remote rows to apply
+    DevArray<int> log_u, rx_u;
+    DevArray<unsigned int> log_em, log_chg, rx_em, rx_chg;
+    DevArray<double> rx_val;
 
     // per-vertex ----------------------------------------------------------
     DevArray<unsigned char> alive, mark, root_gt, owner_rank, migr_from;
@@ -256,6 +263,7 @@ void host_mark(Engine& E, const char* what);
 // lp.cu ---------------------------------------------------------------------
 void lp_run_dev(Engine& E, double delta, long long max_iter, bool itlp);
 void lp_run_actions(Engine& E, double delta, bool first, bool cleanup);
+void lp_rows_apply(Engine& E, long long m, long long r_par);
 void lp_setup(Engine& E);
 void lp_dump_trace(Engine& E, long long rounds);
 void itlp_active_dev(Engine& E, long long n);

@@ -979,7 +979,7 @@ __device__ inline int shard_owner(int root, int world) {
 __global__ void k_eligible(long long n, int ncol, long long cap, const unsigned char* alive, const signed char* gt,
                            const int* par, const unsigned char* root_gt, const int* row_len, unsigned char* mark,
                            unsigned int* eligm, double* f0, double* f1, int* elist, int* f0list, DevState* ds,
-                           int rank, int world, unsigned char* owner_rank, unsigned char* migr_from,
+                           int rank, int world, int rows, unsigned char* owner_rank, unsigned char* migr_from,
                            int* migr_flag) {
     unsigned int allc = ncol >= 32 ? 0xffffffffu : ((1u << ncol) - 1u);
     long long iso = 0, unr = 0;
@@ -987,7 +987,10 @@ __global__ void k_eligible(long long n, int ncol, long long cap, const unsigned 
         bool unl = alive[v] && gt[v] == -1;
         bool reached = alive[v] && root_gt[par[v]];
         bool e = unl && reached;
-        if (world > 1) {  // sharded: only this rank's components are propagated here
+        if (world > 1 && rows) {  // row partition: this rank evaluates the rows v % world == rank
+            e = e && (v % world) == rank;
+            migr_flag[v] = 0;
+        } else if (world > 1) {  // sharded: only this rank's components are propagated here
             int mig = 0;
             if (e) {
                 int o = shard_owner(par[v], world);
@@ -1048,7 +1051,7 @@ void reach_and_pin_dev(Engine& E, bool full_rebuild, long long n) {
     E.launches++;
     k_eligible<<<grid_for(n), kBlock, 0, st>>>(n, E.ncol, E.cap_n, E.alive.p, E.gt.p, E.parent.p, E.root_gt.p,
                                                E.row_len.p, E.mark.p, E.eligm.p, E.f[0].p, E.f[1].p, E.elist.p, E.f0.p,
-                                               E.ds, E.shard_rank, E.shard_world, E.owner_rank.p, E.migr_from.p,
+                                               E.ds, E.shard_rank, E.shard_world, E.shard_rows, E.owner_rank.p, E.migr_from.p,
                                                E.migr_flag.p);
     E.launches++;
 }

@@ -116,6 +116,11 @@ struct LPParams {
     int itlp;
     int action_mode;  // execute ctl->act[] once per column, then exit (sharded batches)
     int cleanup;      // action mode: clear the leftover frontier masks and exit
+    // row-partitioned mode (one round per launch): work-item log of the round
+    // (vertex, evaluated mask, changed mask), exchanged by the host
+    int* log_u;
+    unsigned int* log_em;
+    unsigned int* log_chg;
 };
 
 struct ColState {
@@ -508,6 +513,7 @@ __device__ void warp_tile(const LPParams& P, const RoundCtx& R, ClaimCtx& K, Blo
         unsigned int m = (bal >> (lane * C)) & cmask;
         if (m) {
             K.claimed |= m;  // u changed, so u itself is eligible for those columns
+            if (P.log_chg) P.log_chg[R.ybase + k0 + lane] = m;
             if (R.scan_mode)
                 atomicOr(&K.fm_next[T.u[lane]], m);
             else
@@ -924,6 +930,7 @@ __device__ void cta_hub_row(const LPParams& P, const RoundCtx& R, ClaimCtx& K, B
     if (m) {
         if (tid == 0) {
             K.claimed |= m;
+            if (P.log_chg) P.log_chg[R.ybase + k] = m;
             if (R.scan_mode)
                 atomicOr(&K.fm_next[u], m);
             else
@@ -1177,6 +1184,10 @@ __global__ void __launch_bounds__(kLpThreads, DLP_LP_MINB) k_lp_fused(LPParams P
                 const long long i = i0 + h * gth;
                 const int u = uu[h];
                 if (u < 0) continue;
+                if (P.log_u) {
+                    P.log_u[i] = u;
+                    P.log_em[i] = ee[h];
+                }
                 if (ctl->seen) {
                     int old = atomicExch(&ctl->seen[u], (int)(R + 1));
                     if (old == (int)(R + 1)) atomicAdd(&ctl->dups, 1ULL);
@@ -1254,6 +1265,7 @@ __global__ void __launch_bounds__(kLpThreads, DLP_LP_MINB) k_lp_fused(LPParams P
             }
         }
         if (gtid == 0) {
+            if (P.log_u) ctl->log_n = nwork;
             RoundSlot* nx = &ctl->slot[rn];
             for (int c = 0; c < kMaxCols; c++) nx->rmax[c] = nx->neval[c] = nx->edges[c] = nx->warn[c] = 0;
             nx->claimed = 0;
@@ -1403,6 +1415,8 @@ void lp_run_dev(Engine& E, double delta, long long max_iter, bool itlp) {
     P.itlp = itlp ? 1 : 0;
     P.action_mode = 0;
     P.cleanup = 0;
+    P.log_u = nullptr;
+    P.log_em = P.log_chg = nullptr;
     DLP_CUDA_TRY(cudaMemsetAsync(E.ctl, 0, sizeof(LPCtl), E.st));
     if (E.lp_trace_path) {
         const long long cap = 1 << 16;
@@ -1461,6 +1475,21 @@ void lp_run_actions(Engine& E, double delta, bool first, bool cleanup) {
     P.itlp = 0;
     P.action_mode = 1;
     P.cleanup = cleanup ? 1 : 0;
+    P.log_u = nullptr;
+    P.log_em = P.log_chg = nullptr;
+    const bool rows = E.shard_rows && E.shard_world > 1;
+    if (rows) {  // one round per launch; its work items are logged for the exchange
+        const size_t nn = (size_t)E.cap_n + 1;
+        if (E.log_chg.n < nn) {
+            E.log_chg.reserve(nn, 0, E.st);
+            DLP_CUDA_TRY(cudaMemsetAsync(E.log_chg.p, 0, E.log_chg.n * sizeof(unsigned int), E.st));
+        }
+        E.log_u.reserve(nn, 0, E.st);
+        E.log_em.reserve(nn, 0, E.st);
+        P.log_u = E.log_u.p;
+        P.log_em = E.log_em.p;
+        P.log_chg = E.log_chg.p;
+    }
     if (first) {
         // keep the host-written actions across the reset
         DLP_CUDA_TRY(cudaMemsetAsync(E.ctl, 0, offsetof(LPCtl, act), E.st));
@@ -1468,9 +1497,49 @@ void lp_run_actions(Engine& E, double delta, bool first, bool cleanup) {
     } else {
         DLP_CUDA_TRY(cudaMemsetAsync(&E.ctl->bar, 0, sizeof(unsigned int), E.st));
     }
+    if (rows) DLP_CUDA_TRY(cudaMemsetAsync(&E.ctl->log_n, 0, sizeof(long long), E.st));
     void* args[] = {&P};
     DLP_CUDA_TRY(cudaLaunchCooperativeKernel((void*)k_lp_fused, dim3(E.lp_grid), dim3(kLpThreads), args, E.lp_smem,
                                              E.st));
+    E.launches++;
+}
+
+// Row-partitioned mode: apply the rows other ranks evaluated in the last
+// round -- their committed labels, and the claims their changed rows make on
+// this rank's vertices (the eligible mask holds only owned vertices) -- into
+// the next round's frontier lists, as if this rank's own rows had changed.
+// One warp per remote row.
+__global__ void k_rows_apply(long long m, int C, const int* ru, const unsigned int* rem, const unsigned int* rchg,
+                             const double* rval, double* X, const long long* row_start, const int* row_len,
+                             const int* nbr, ClaimCtx K, int* has_fr) {
+    const int lane = threadIdx.x & 31;
+    const long long wid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long i = wid; i < m; i += nw) {
+        const int u = ru[i];
+        const unsigned int em = rem[i], chg = rchg[i];
+        for (int c = lane; c < C; c += 32)
+            if ((em >> c) & 1u) X[(long long)u * C + c] = rval[i * C + c];
+        if (!chg) continue;
+        if (lane == 0) claim(K, u, chg);
+        const long long st = row_start[u];
+        const int len = row_len[u];
+        for (int t = lane; t < len; t += 32) claim(K, nbr[st + t], chg);
+    }
+    for (int c = 0; c < C; c++)
+        if ((K.claimed >> c) & 1u) has_fr[c] = 1;
+}
+
+void lp_rows_apply(Engine& E, long long m, long long r_par) {
+    if (m <= 0) return;
+    const int ri = (int)(r_par & 1);
+    ClaimCtx K{E.fmask[ri].p, {E.ulist[ri].p, E.llist[ri].p, E.hlist[ri].p}, E.ctl->ncur_p, E.eligm.p, E.row_len.p,
+               0u, 0ULL, 0ULL, 0u, 0.0};
+    const long long blocks = std::min<long long>((m * 32 + kBlock - 1) / kBlock, (long long)E.sm_count * 16);
+    k_rows_apply<<<(unsigned int)blocks, kBlock, 0, E.st>>>(m, E.ncol, E.rx_u.p, E.rx_em.p, E.rx_chg.p, E.rx_val.p,
+                                                           E.f[0].p, E.row_start.p, E.row_len.p, E.nbr.p, K,
+                                                           E.ctl->has_fr);
+    DLP_CUDA_TRY(cudaGetLastError());
     E.launches++;
 }
 

@@ -10,6 +10,12 @@ frontier non-empty, eligible counts): a few bytes per phase, reduced with the
 caller's collective (NCCL all-reduce over NVLink with torch.distributed, or an
 in-process reduction for virtual shards on one device).  Reports are the
 global ones; labels of a vertex live on the rank that last propagated it.
+
+mode="rows" partitions the rows instead (rank r evaluates v % world == r),
+for a stream dominated by one giant component: every global round ends with
+an all-gather of the evaluated rows (vertex, masks, new labels) and each rank
+applies the other ranks' labels and frontier claims, so labels are
+replicated on every rank.
 """
 
 from __future__ import annotations
@@ -76,10 +82,16 @@ class InProcessCollective:
 class ShardedGraph(DynamicGraph):
     """DynamicGraph holding this rank's share of the propagation."""
 
-    def __init__(self, device: int, num_classes: int, rank: int, world: int, collective: Collective) -> None:
+    MODES = {"components": 0, "rows": 1}
+
+    def __init__(self, device: int, num_classes: int, rank: int, world: int, collective: Collective,
+                 mode: str = "components") -> None:
         super().__init__(device, num_classes)
-        self.rank, self.world = int(rank), int(world)
+        if mode not in self.MODES:
+            raise ValueError(f"unknown shard mode {mode!r}")
+        self.rank, self.world, self.mode = int(rank), int(world), mode
         self._check(self._lib.dlp_shard_set(self._h, self.rank, self.world))
+        self._check(self._lib.dlp_shard_mode(self._h, self.MODES[mode]))
         self._collective = collective
 
         def cb(ctx, imax, nimax, isum, nisum, dmax, ndmax):
@@ -150,11 +162,11 @@ def gather_labels(graph: ShardedGraph, group=None, device=None) -> np.ndarray:
 
 
 def run_virtual_shards(batches, cfg: EngineConfig, world: int, num_classes: int = 2, device: int = 0,
-                       on_batch: Optional[Callable] = None):
+                       on_batch: Optional[Callable] = None, mode: str = "components"):
     """Run a stream as `world` component shards on ONE device (threads +
     in-process reduction): the sharded protocol without NCCL, for tests."""
     coll = InProcessCollective(world)
-    graphs = [ShardedGraph(device, num_classes, r, world, coll.for_rank(r)) for r in range(world)]
+    graphs = [ShardedGraph(device, num_classes, r, world, coll.for_rank(r), mode) for r in range(world)]
     labels = [LabelState() for _ in range(world)]
     out = []
     for b in batches:
@@ -175,6 +187,10 @@ def run_virtual_shards(batches, cfg: EngineConfig, world: int, num_classes: int 
         if errs:
             raise errs[0]
         F = merge_labels([(g.read_labels()[0], g.owned()) for g in graphs])
+        if mode == "rows":  # labels are replicated: every rank holds the whole matrix
+            for g in graphs[1:]:
+                if not np.array_equal(g.read_labels()[0].view(np.int64), F.view(np.int64)):
+                    raise RuntimeError(f"row-partitioned rank {g.rank} diverged from the merged labels")
         out.append((res[0], F))
         if on_batch:
             on_batch(res, F)

@@ -94,6 +94,11 @@ def _stream(kind):
         e = streams.knn_graph_exact(bl.x, 8)
         gt = streams.stratified_seeds(bl.classes, 0.02, 3)
         return streams.phased_stream(5000, e, bl.classes, gt, 500, 3, 0.75, 0.02, 0.23, initial_gt=20).batches, 10
+    if kind == "giant":  # overlapping classes: one giant component (row partition's case)
+        bl = streams.make_blobs(6000, 8, 3, 5, spread=1.0)
+        e = streams.knn_graph_exact(bl.x, 10)
+        gt = streams.stratified_seeds(bl.classes, 0.02, 5)
+        return streams.phased_stream(6000, e, bl.classes, gt, 600, 5, 0.7, 0.02, 0.28, initial_gt=6).batches, 3
     bl = streams.make_blobs(4000, 8, 2, 4, spread=30.0)
     e = streams.knn_graph_exact(bl.x, 6)
     gt = streams.stratified_seeds(bl.classes, 0.02, 4)
@@ -101,15 +106,17 @@ def _stream(kind):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("kind,world", [("blobs2", 2), ("blobs10", 2), ("blobs10", 3)])
-def test_virtual_shards_bit_identical(gpu_device, kind, world):
+@pytest.mark.parametrize("kind,world,mode", [("blobs2", 2, "components"), ("blobs10", 2, "components"),
+                                             ("blobs10", 3, "components"), ("blobs2", 2, "rows"),
+                                             ("blobs10", 3, "rows"), ("giant", 2, "rows"), ("giant", 4, "rows")])
+def test_virtual_shards_bit_identical(gpu_device, kind, world, mode):
     from paper_2604_06596_b200.engine import EngineConfig
     from paper_2604_06596_b200.sharded import run_virtual_shards
 
     batches, ncls = _stream(kind)
     cfg = EngineConfig(delta=1e-5)
     want = _unsharded(batches, cfg, ncls)
-    got = run_virtual_shards(batches, cfg, world, num_classes=ncls)
+    got = run_virtual_shards(batches, cfg, world, num_classes=ncls, mode=mode)
     for t, ((rw, Fw), (rg, Fg)) in enumerate(zip(want, got)):
         rg = rg if isinstance(rg, list) else [rg]
         for c, (a, b) in enumerate(zip(rw, rg)):
