@@ -41,6 +41,16 @@ __device__ inline bool is_boxed(double x) { return x != x; }
 __device__ inline int boxed_class(double x) { return (int)(__double_as_longlong(x) & 1); }
 __device__ inline double unbox(double x) { return is_boxed(x) ? (double)boxed_class(x) : x; }
 
+// Shared-memory load that ptxas keeps in program order with its peers: a
+// block of these issues back to back instead of being sunk next to each use
+// (under the kernel's register cap the scheduler otherwise serialises
+// load -> term -> sum per entry).
+__device__ inline double lds64(const double* p) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"((unsigned int)__cvta_generic_to_shared(p)));
+    return v;
+}
+
 // ---------------------------------------------------------------------------
 // The per-vertex update of _csr.pyx:24-58 with the reference's exact
 // operation order; explicit round-to-nearest intrinsics (and --fmad=false)
@@ -72,6 +82,35 @@ struct RowAcc {
         w0 = __dadd_rn(w0, (gt && cls == 0) ? w : 0.0);
         w1 = __dadd_rn(w1, (gt && cls == 1) ? w : 0.0);
         s = __dadd_rn(s, gt ? 0.0 : p);
+    }
+    // B consecutive entries (x strided by xs): the per-entry terms first
+    // (independent of the sums, so they overlap), then the four chains -- the
+    // same operations in the same order as B calls of add_boxed
+    template <int B>
+    __device__ inline void add_boxed_block(const double* w, const double* x, int xs, double fu) {
+        double wv[B], t0[B], t1[B], ts[B];
+#pragma unroll
+        for (int j = 0; j < B; j++) {
+            wv[j] = lds64(w + j);
+            t0[j] = lds64(x + j * xs);
+        }
+#pragma unroll
+        for (int j = 0; j < B; j++) {
+            const double xv = t0[j];
+            const bool gt = is_boxed(xv);
+            const int cls = boxed_class(xv);
+            const double p = __dmul_rn(__dsub_rn(xv, fu), wv[j]);
+            t0[j] = (gt && cls == 0) ? wv[j] : 0.0;
+            t1[j] = (gt && cls == 1) ? wv[j] : 0.0;
+            ts[j] = gt ? 0.0 : p;
+        }
+#pragma unroll
+        for (int j = 0; j < B; j++) {
+            w_all = __dadd_rn(w_all, wv[j]);
+            w0 = __dadd_rn(w0, t0[j]);
+            w1 = __dadd_rn(w1, t1[j]);
+            s = __dadd_rn(s, ts[j]);
+        }
     }
     // returns |fn - fu| or -1 for the isolated sentinel (value 0.5)
     __device__ inline double finish(double fu, double* out_val) const {

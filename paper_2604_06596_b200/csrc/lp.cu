@@ -369,6 +369,7 @@ struct RoundCtx {
     unsigned int FR, CE;    // column actions of the round
     const unsigned int* fm_cur;
     bool scan_mode;         // expand by fire-and-forget atomicOr + compaction
+    unsigned long long* tmax;  // trace: longest evaluated row of the round (or null)
 };
 
 // Evaluate `nrows` consecutive work items W[k0 ..] as one warp tile:
@@ -419,6 +420,7 @@ __device__ void warp_tile(const LPParams& P, const RoundCtx& R, ClaimCtx& K, Blo
         if (lane >= o) incl += y;
     }
     if (lane < nrows) T.off[lane] = incl - len;
+    if (R.tmax && len) atomicMax(R.tmax, (unsigned long long)len);
     const int total = __shfl_sync(0xffffffffu, incl, 31);
     {
         unsigned int nz = __ballot_sync(0xffffffffu, em != 0);
@@ -475,8 +477,9 @@ __device__ void warp_tile(const LPParams& P, const RoundCtx& R, ClaimCtx& K, Blo
         if (aact) {
             const double fu = sfu[ar * C + ac];
             const int lo = max(a_lo, wb) - wb, hi = min(a_hi, wb + wn) - wb;
-#pragma unroll kAccUnroll
-            for (int t = lo; t < hi; t++) acc.add_boxed(sw[t], sx[t * C + ac], fu);
+            int t = lo;
+            for (; t + kAccUnroll <= hi; t += kAccUnroll) acc.add_boxed_block<kAccUnroll>(sw + t, sx + t * C + ac, C, fu);
+            for (; t < hi; t++) acc.add_boxed(sw[t], sx[t * C + ac], fu);
         }
         __syncwarp();
     }
@@ -868,6 +871,7 @@ __device__ void cta_hub_row(const LPParams& P, const RoundCtx& R, ClaimCtx& K, B
         s_i[1] = em ? P.row_len[u] : 0;
         s_ll[0] = em ? P.row_start[u] : 0;
         if (em) {
+            if (R.tmax) atomicMax(R.tmax, (unsigned long long)s_i[1]);
             atomicAdd(&B.urows, 1ULL);
             atomicAdd(&B.uent, (unsigned long long)s_i[1]);
         }
@@ -881,38 +885,162 @@ __device__ void cta_hub_row(const LPParams& P, const RoundCtx& R, ClaimCtx& K, B
     __syncthreads();
     const int nwin = (len + kHubWin - 1) / kHubWin;
     const int bsz = kHubWin * (C + 1);
-    auto gather = [&](int w, int t0, int nth) {
+    // warps 0-3 run the row's four ordered sums (RowAcc::add_boxed split by
+    // accumulator: s, w_all, w0, w1; lane c = column c), so the sequential
+    // chains advance in parallel on four schedulers; warps 4-7 gather.  A
+    // gathering thread holds the ids and weights of its entries of the window
+    // after next in registers, so a window's gather is one round trip.
+    constexpr int kSumWarps = 4;
+    constexpr int kGth = kLpThreads - 32 * kSumWarps;
+    constexpr int kPer = (kHubWin + kGth - 1) / kGth;
+    const int g = tid - 32 * kSumWarps;
+    int pv[kPer];
+    double pw[kPer];
+    auto load_ids = [&](int w) {
+        const int wb = w * kHubWin, wn = min(kHubWin, len - wb);
+#pragma unroll
+        for (int j = 0; j < kPer; j++) {
+            const int i = g + kGth * j;
+            if (i < wn) {
+                pv[j] = __ldcs(P.nbr + st + wb + i);
+                pw[j] = __ldcs(P.w + st + wb + i);
+            }
+        }
+    };
+    auto issue = [&](int w) {
         double* sw = buf + (w & 1) * bsz;
         double* sx = sw + kHubWin;
-        const int wb = w * kHubWin, wn = min(kHubWin, len - wb);
-        for (int i = t0; i < wn; i += nth) {
-            long long p = st + wb + i;
-            int v = __ldcs(P.nbr + p);
-            sw[i] = __ldcs(P.w + p);
-            copy_label_row(sx + i * C, P.X + (long long)v * C, C, pol);
+        const int wn = min(kHubWin, len - w * kHubWin);
+#pragma unroll
+        for (int j = 0; j < kPer; j++) {
+            const int i = g + kGth * j;
+            if (i < wn) {
+                sw[i] = pw[j];
+                copy_label_row(sx + i * C, P.X + (long long)pv[j] * C, C, pol);
+            }
         }
-        cp_async_wait_all();
     };
-    gather(0, tid, kLpThreads);
-    __syncthreads();
-    const bool act = tid < C && ((em >> tid) & 1u);
-    RowAcc acc;
-    acc.init();
-    for (int w = 0; w < nwin; w++) {
-        if (warp != 0) {
-            if (w + 1 < nwin) gather(w + 1, tid - 32, kLpThreads - 32);
-        } else if (act) {
-            const double* sw = buf + (w & 1) * bsz;
-            const double* sx = sw + kHubWin;
-            const int wn = min(kHubWin, len - w * kHubWin);
-            const double fu = s_fu[tid];
-            for (int t = 0; t < wn; t++) acc.add_boxed(sw[t], sx[t * C + tid], fu);
-        }
-        __syncthreads();
+    if (warp >= kSumWarps) {
+        load_ids(0);
+        issue(0);
+        if (nwin > 1) load_ids(1);
+        cp_async_wait_all();
     }
-    if (act) {
+    __syncthreads();
+    const bool act = warp < kSumWarps && lane < C && ((em >> lane) & 1u);
+    const double fu = act ? s_fu[lane] : 0.0;
+    double acc = 0.0;
+#ifdef DLP_HUBPROF
+    // diagnostics: cycles per part of the hub loop (warp 4 and warps 0-3, lane 0)
+    long long hp[3] = {0, 0, 0};
+#define HUBT(v) long long v = clock64()
+#else
+#define HUBT(v)
+#endif
+    for (int w = 0; w < nwin; w++) {
+        HUBT(ta);
+        if (warp >= kSumWarps) {
+            if (w + 1 < nwin) {
+                issue(w + 1);
+                if (w + 2 < nwin) load_ids(w + 2);
+                HUBT(tb);
+                cp_async_wait_all();
+#ifdef DLP_HUBPROF
+                hp[0] += tb - ta;
+                hp[1] += clock64() - tb;
+#endif
+            }
+        } else if (act) {
+            // shared loads run a block of 8 entries ahead of the chain
+            const double* sw = buf + (w & 1) * bsz;
+            const double* sx = sw + kHubWin + lane;
+            const int wn = min(kHubWin, len - w * kHubWin);
+            if (warp == 1) {  // w_all
+                int t = 0;
+                for (; t + 8 <= wn; t += 8) {
+                    double wv[8];
+#pragma unroll
+                    for (int j = 0; j < 8; j++) wv[j] = sw[t + j];
+#pragma unroll
+                    for (int j = 0; j < 8; j++) acc = __dadd_rn(acc, wv[j]);
+                }
+                for (; t < wn; t++) acc = __dadd_rn(acc, sw[t]);
+            } else if (warp == 0) {  // s: the label-difference sum
+                // terms of a block first (independent), then the chain
+                int t = 0;
+                for (; t + 8 <= wn; t += 8) {
+                    double tv[8], xv[8], wv[8];
+#pragma unroll
+                    for (int j = 0; j < 8; j++) {
+                        xv[j] = lds64(sx + (t + j) * C);
+                        wv[j] = lds64(sw + t + j);
+                    }
+#pragma unroll
+                    for (int j = 0; j < 8; j++) {
+                        const double p = __dmul_rn(__dsub_rn(xv[j], fu), wv[j]);
+                        tv[j] = is_boxed(xv[j]) ? 0.0 : p;
+                    }
+#pragma unroll
+                    for (int j = 0; j < 8; j++) acc = __dadd_rn(acc, tv[j]);
+                }
+                for (; t < wn; t++) {
+                    const double x = sx[t * C];
+                    acc = __dadd_rn(acc, is_boxed(x) ? 0.0 : __dmul_rn(__dsub_rn(x, fu), sw[t]));
+                }
+            } else {  // warp 2: w0, warp 3: w1 (weights of ground-truth neighbours per class)
+                const int cls_want = warp - 2;
+                int t = 0;
+                for (; t + 8 <= wn; t += 8) {
+                    double tv[8], xv[8], wv[8];
+#pragma unroll
+                    for (int j = 0; j < 8; j++) {
+                        xv[j] = lds64(sx + (t + j) * C);
+                        wv[j] = lds64(sw + t + j);
+                    }
+#pragma unroll
+                    for (int j = 0; j < 8; j++)
+                        tv[j] = (is_boxed(xv[j]) && boxed_class(xv[j]) == cls_want) ? wv[j] : 0.0;
+#pragma unroll
+                    for (int j = 0; j < 8; j++) acc = __dadd_rn(acc, tv[j]);
+                }
+                for (; t < wn; t++) {
+                    const double x = sx[t * C];
+                    acc = __dadd_rn(acc, (is_boxed(x) && boxed_class(x) == cls_want) ? sw[t] : 0.0);
+                }
+            }
+#ifdef DLP_HUBPROF
+            hp[0] += (long long)(__double_as_longlong(acc) & 0) + clock64() - ta;  // keep the chain before the stamp
+#endif
+        }
+        HUBT(tc);
+        __syncthreads();
+#ifdef DLP_HUBPROF
+        hp[2] += clock64() - tc;
+#endif
+    }
+#ifdef DLP_HUBPROF
+    if (lane == 0 && P.ctl->prof) {
+        if (warp == kSumWarps) {
+            atomicAdd(&P.ctl->prof[0], (unsigned long long)hp[0]);
+            atomicAdd(&P.ctl->prof[1], (unsigned long long)hp[1]);
+            atomicAdd(&P.ctl->prof[2], (unsigned long long)hp[2]);
+        } else if (warp < kSumWarps) {
+            atomicAdd(&P.ctl->prof[3 + warp], (unsigned long long)hp[0]);
+            if (warp == 0) atomicAdd(&P.ctl->prof[7], (unsigned long long)hp[2]);
+        }
+    }
+#endif
+    double* chains = buf;  // [4][kMaxCols]: the windows are free now
+    if (act) chains[warp * kMaxCols + lane] = acc;
+    __syncthreads();
+    if (tid < C && ((em >> tid) & 1u)) {
+        RowAcc ra;
+        ra.s = chains[tid];
+        ra.w_all = chains[kMaxCols + tid];
+        ra.w0 = chains[2 * kMaxCols + tid];
+        ra.w1 = chains[3 * kMaxCols + tid];
         double val;
-        double d = acc.finish(s_fu[tid], &val);
+        double d = ra.finish(s_fu[tid], &val);
         __stcs(P.Y + (R.ybase + k) * C + tid, val);
         atomicAdd(&B.neval[tid], 1ULL);
         atomicAdd(&B.edges[tid], (unsigned long long)len);
@@ -1088,7 +1216,8 @@ __global__ void __launch_bounds__(kLpThreads, DLP_LP_MINB) k_lp_fused(LPParams P
         // ======== phase 1: evaluate + expand ========
         // staging items: short [0, n0c), long [n0c, n0c+n1c), hub [n0c+n1c, nwork)
         {
-            RoundCtx RH{W2, n0c + n1c, FR, CE, fm_cur, scan_mode};
+            unsigned long long* tmax = (ctl->trace && R < ctl->trace_cap) ? ctl->trace + 8 * R + 7 : nullptr;
+            RoundCtx RH{W2, n0c + n1c, FR, CE, fm_cur, scan_mode, tmax};
             unsigned long long tw1 = 0, tw2 = 0, tw3 = 0;
 #ifdef DLP_PROF
             const bool prof = ctl->prof != nullptr && lane == 0;
@@ -1107,8 +1236,8 @@ __global__ void __launch_bounds__(kLpThreads, DLP_LP_MINB) k_lp_fused(LPParams P
                     cta_hub_row(P, RH, K, B, smem_dyn, s_fu, k, pol, s_i, s_ll, s_u32);
                 }
             }
-            RoundCtx RL{W1, n0c, FR, CE, fm_cur, scan_mode};
-            RoundCtx RS{W0, 0, FR, CE, fm_cur, scan_mode};
+            RoundCtx RL{W1, n0c, FR, CE, fm_cur, scan_mode, tmax};
+            RoundCtx RS{W0, 0, FR, CE, fm_cur, scan_mode, tmax};
 #ifdef DLP_PC
             if (warp < 4) {
                 pc_produce_class(P, RL, &slot->grab[1], n1c, 1, ring, pol);  // long rows: one per tile
@@ -1421,6 +1550,7 @@ void lp_run_dev(Engine& E, double delta, long long max_iter, bool itlp) {
     if (E.lp_trace_path) {
         const long long cap = 1 << 16;
         E.lp_trace.reserve(8 * cap + 8, 0, E.st);
+        DLP_CUDA_TRY(cudaMemsetAsync(E.lp_trace.p, 0, (8 * cap + 8) * sizeof(unsigned long long), E.st));
         unsigned long long* tp = E.lp_trace.p;
         DLP_CUDA_TRY(cudaMemcpyAsync(&E.ctl->trace, &tp, sizeof(tp), cudaMemcpyHostToDevice, E.st));
         DLP_CUDA_TRY(cudaMemcpyAsync(&E.ctl->trace_cap, &cap, sizeof(cap), cudaMemcpyHostToDevice, E.st));
@@ -1553,11 +1683,13 @@ void lp_dump_trace(Engine& E, long long rounds) {
     if (!fp) return;
     unsigned long long pr[8] = {0};
     DLP_CUDA_TRY(cudaMemcpy(pr, E.lp_prof.p, sizeof(pr), cudaMemcpyDeviceToHost));
-    fprintf(fp, "# launch rounds=%lld grid=%d dups=%llu prof_ms(warp-sum) hub=%.1f long=%.1f short=%.1f phase1=%.1f\n",
-            rounds, E.lp_grid, E.h_ctl.p->dups, pr[0] / 1e6, pr[1] / 1e6, pr[2] / 1e6, pr[3] / 1e6);
+    fprintf(fp, "# launch rounds=%lld grid=%d dups=%llu prof_ms(warp-sum) hub=%.1f long=%.1f short=%.1f phase1=%.1f"
+            " raw %llu %llu %llu %llu %llu %llu %llu %llu\n",
+            rounds, E.lp_grid, E.h_ctl.p->dups, pr[0] / 1e6, pr[1] / 1e6, pr[2] / 1e6, pr[3] / 1e6, pr[0], pr[1],
+            pr[2], pr[3], pr[4], pr[5], pr[6], pr[7]);
     for (long long r = 0; r < n; r++)
-        fprintf(fp, "%lld %llu %llu %llx %llu %llu %llu %llu\n", r, h[8 * r], h[8 * r + 1], h[8 * r + 2],
-                h[8 * r + 3], h[8 * r + 4], h[8 * r + 5], h[8 * r + 6]);
+        fprintf(fp, "%lld %llu %llu %llx %llu %llu %llu %llu %llu\n", r, h[8 * r], h[8 * r + 1], h[8 * r + 2],
+                h[8 * r + 3], h[8 * r + 4], h[8 * r + 5], h[8 * r + 6], h[8 * r + 7]);
     fclose(fp);
 }
 

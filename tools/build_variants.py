@@ -6,12 +6,19 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2604_06596_b200 import build  # noqa: E402
 
 VARIANTS = {
-    "ca": ["DLP_CP_CA"],
-    "nohint": ["DLP_CP_NOHINT"],
-    "pc_ca": ["DLP_PC", "DLP_CP_CA"],
+    "u8": ["DLP_ACC_UNROLL=8"],
+    "hubprof": ["DLP_HUBPROF"],
+    "minb2": ["DLP_LP_MINB=2"],
+    "minb2hp": ["DLP_LP_MINB=2", "DLP_HUBPROF"],
+    "minb4": ["DLP_LP_MINB=4"],
+    "minb4w32": ["DLP_LP_MINB=4", "DLP_WIN=32"],
+    "w32": ["DLP_WIN=32"],
 }
 if __name__ == "__main__":
     root = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "scratch")
     os.makedirs(root, exist_ok=True)
+    only = sys.argv[1:]
     for name, d in VARIANTS.items():
+        if only and name not in only:
+            continue
         print(name, build.build(force=True, defines=d, out=os.path.join(root, f"lib_{name}.so")))

@@ -17,7 +17,8 @@ def launches(path):
         r, ns, nl, m, t = f[:5]
         p1, r0 = (int(f[5]), int(f[6])) if len(f) >= 7 else (0, 0)
         ue = int(f[7]) if len(f) >= 8 else 0
-        cur.append((int(r), int(ns), int(nl), int(m, 16), int(t), p1, r0, ue))
+        ml = int(f[8]) if len(f) >= 9 else 0
+        cur.append((int(r), int(ns), int(nl), int(m, 16), int(t), p1, r0, ue, ml))
     if cur:
         out.append(np.array(cur, dtype=np.float64))
     return out
@@ -56,6 +57,15 @@ def summarise(a):
             if sel.any():
                 print(f"    entries [{lo:.0e},{hi:.0e}): rounds {sel.sum()}, phase1 total {ph1[sel].sum() / 1e3:.2f} ms, "
                       f"{ent[sel].sum() / max(ph1[sel].sum(), 1e-9) / 1e3:.2f} G entries/s")
+    if a.shape[1] >= 9 and a[:, 8].sum() > 0:
+        ph1 = (a[:, 5] - a[:, 6]) / 1e3
+        ml = a[:, 8]
+        print("    small rounds (< 1e5 entries) by longest row:")
+        for lo, hi in [(0, 96), (96, 384), (384, 1000), (1000, 2000), (2000, 1e9)]:
+            sel = (ml >= lo) & (ml < hi) & (a[:, 7] < 1e5) & (~ce)
+            if sel.any():
+                print(f"      longest [{lo:.0f},{hi:.0f}): rounds {sel.sum()}, phase1 median {np.median(ph1[sel]):.1f} us, "
+                      f"total {ph1[sel].sum() / 1e3:.2f} ms, ns per longest entry {np.median(ph1[sel] * 1e3 / ml[sel]):.1f}")
     if ce.any():
         print(f"  certify: us/round={dt[ce].mean():.1f} rows/round={rows[ce].mean():.0f} "
               f"long/round={nlong[ce].mean():.0f} hub/round={nhub[ce].mean():.0f}")
