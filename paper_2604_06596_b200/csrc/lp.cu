@@ -53,7 +53,7 @@ namespace dlp {
 
 constexpr int kLpThreads = 256;
 #ifndef DLP_WIN
-#define DLP_WIN 64
+#define DLP_WIN 32
 #endif
 #ifndef DLP_HUB_WIN
 #define DLP_HUB_WIN 256

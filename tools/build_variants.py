@@ -6,13 +6,16 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2604_06596_b200 import build  # noqa: E402
 
 VARIANTS = {
-    "u8": ["DLP_ACC_UNROLL=8"],
     "hubprof": ["DLP_HUBPROF"],
     "minb2": ["DLP_LP_MINB=2"],
     "minb2hp": ["DLP_LP_MINB=2", "DLP_HUBPROF"],
     "minb4": ["DLP_LP_MINB=4"],
     "minb4w32": ["DLP_LP_MINB=4", "DLP_WIN=32"],
     "w32": ["DLP_WIN=32"],
+    "w64": ["DLP_WIN=64"],
+    "lp2": ["DLP_LONG_PER=2"],
+    "u2": ["DLP_ACC_UNROLL=2"],
+    "u8": ["DLP_ACC_UNROLL=8"],
 }
 if __name__ == "__main__":
     root = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "scratch")
