@@ -13,6 +13,8 @@ VARIANTS = {
     "minb4w32": ["DLP_LP_MINB=4", "DLP_WIN=32"],
     "w32": ["DLP_WIN=32"],
     "w64": ["DLP_WIN=64"],
+    "sel": ["DLP_SUMS_SELECT"],
+    "pred": ["DLP_SUMS_PRED"],
     "lp2": ["DLP_LONG_PER=2"],
     "u2": ["DLP_ACC_UNROLL=2"],
     "u8": ["DLP_ACC_UNROLL=8"],
