@@ -167,8 +167,20 @@ BatchDev stage_batch(Engine& E, const HostBatch& b, int slot = 0, cudaStream_t s
         tot += align_up(sz[i]);
     }
     off[6] = tot;
-    hs.reserve(tot + 256);
-    ds.reserve(tot + 256, 0, st);
+    // both staging slots grow together, with a floor, so the ingestion
+    // pipeline never allocates pinned memory (or its copy stream) mid-stream
+    const size_t want = std::max(tot + 256, (size_t)32 << 20);
+    if (hs.n < tot + 256) {
+        E.h_stage.reserve(want);
+        E.h_stage2.reserve(want);
+        E.d_stage.reserve(want, 0, E.st);
+        E.d_stage2.reserve(want, 0, E.st);
+        DLP_CUDA_TRY(cudaStreamSynchronize(E.st));  // the device slots exist before any copy stream uses them
+    }
+    if (!E.cst) {
+        DLP_CUDA_TRY(cudaStreamCreateWithFlags(&E.cst, cudaStreamNonBlocking));
+        DLP_CUDA_TRY(cudaEventCreateWithFlags(&E.cev, cudaEventDisableTiming));
+    }
     const void* src[6] = {b.ids, b.gt, b.owner, b.other, b.w, b.dels};
     for (int i = 0; i < 6; i++)
         if (sz[i]) memcpy(hs.p + off[i], src[i], sz[i]);
@@ -814,6 +826,7 @@ int dlp_destroy(dlp_engine* h) {
     Engine& E = h->E;
     cudaSetDevice(E.device);
     cudaStreamSynchronize(E.st);
+    if (E.l2_persist) cudaCtxResetPersistingL2Cache();  // hand the carve-out's lines back
     DevArray<unsigned char>* u8s[] = {&E.alive, &E.mark, &E.root_gt, &E.owner_rank, &E.migr_from, &E.d_stage,
                                       &E.cub_tmp};
     E.migr_flag.release();

@@ -233,6 +233,9 @@ struct Engine {
     LPCtl* ctl = nullptr;
     PinnedArray<LPCtl> h_ctl;
     int lp_grid = 0;
+    int l2_mode = 1;            // label L2 residency: 0 none, 1 persisting carve-out, 2 + access window
+    size_t l2_persist = 0;      // persisting L2 carve-out (bytes)
+    size_t l2_window_max = 0;
     DevArray<unsigned long long> lp_trace;
     DevArray<int> lp_seen;
     DevArray<unsigned long long> lp_prof;

@@ -43,6 +43,7 @@
 #include <cstddef>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "engine.cuh"
@@ -1486,8 +1487,39 @@ __global__ void __launch_bounds__(kLpThreads, DLP_LP_MINB) k_lp_fused(LPParams P
     }
 }
 
+// Keep the label matrix X resident in L2 across rounds: the gathers re-read
+// it ~|E|/|V| times per round while the adjacency streams past it.  A
+// persisting carve-out (cudaLimitPersistingL2CacheSize) makes the loads'
+// evict_last hints effective, and an access-policy window on the engine's
+// stream marks X itself persisting (the rest streams).  DLP_L2_PERSIST=0/1/2.
+void l2_setup(Engine& E) {
+    if (const char* v = getenv("DLP_L2_PERSIST")) E.l2_mode = atoi(v);
+    if (E.l2_mode <= 0) return;
+    int maxp = 0, maxw = 0;
+    DLP_CUDA_TRY(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, E.device));
+    DLP_CUDA_TRY(cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, E.device));
+    E.l2_persist = (size_t)maxp;
+    E.l2_window_max = (size_t)maxw;
+    if (E.l2_persist) DLP_CUDA_TRY(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, E.l2_persist));
+}
+
+void l2_window(Engine& E, cudaStream_t st) {
+    if (E.l2_mode < 2 || !E.l2_persist || !E.l2_window_max) return;
+    const size_t bytes = std::min((size_t)E.n_slots * E.ncol * sizeof(double), E.l2_window_max);
+    if (!bytes) return;
+    cudaStreamAttrValue v;
+    memset(&v, 0, sizeof(v));
+    v.accessPolicyWindow.base_ptr = (void*)E.f[0].p;
+    v.accessPolicyWindow.num_bytes = bytes;
+    v.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)E.l2_persist / (double)bytes);
+    v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    DLP_CUDA_TRY(cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &v));
+}
+
 void lp_setup(Engine& E) {
     if (E.lp_grid) return;
+    l2_setup(E);
     if (E.ncol > kMaxCols) throw CudaFailure(cudaErrorInvalidValue, "ncol > kMaxCols", __FILE__, __LINE__);
     E.lp_smem = std::max((size_t)(kLpThreads / 32) * (kWin * (E.ncol + 1) + 32),
                          (size_t)2 * kHubWin * (E.ncol + 1)) * sizeof(double);
@@ -1566,6 +1598,7 @@ void lp_run_dev(Engine& E, double delta, long long max_iter, bool itlp) {
     }
     void* args[] = {&P};
     DLP_CUDA_TRY(cudaEventRecord(E.lp_ev[0], E.st));
+    l2_window(E, E.st);
     DLP_CUDA_TRY(cudaLaunchCooperativeKernel((void*)k_lp_fused, dim3(E.lp_grid), dim3(kLpThreads), args, E.lp_smem,
                                              E.st));
     DLP_CUDA_TRY(cudaEventRecord(E.lp_ev[1], E.st));
@@ -1629,6 +1662,7 @@ void lp_run_actions(Engine& E, double delta, bool first, bool cleanup) {
     }
     if (rows) DLP_CUDA_TRY(cudaMemsetAsync(&E.ctl->log_n, 0, sizeof(long long), E.st));
     void* args[] = {&P};
+    l2_window(E, E.st);
     DLP_CUDA_TRY(cudaLaunchCooperativeKernel((void*)k_lp_fused, dim3(E.lp_grid), dim3(kLpThreads), args, E.lp_smem,
                                              E.st));
     E.launches++;
