@@ -114,8 +114,43 @@ struct RowAcc {
     // B calls of add_boxed
     template <int B>
     __device__ inline void add_boxed_block(const double* w, const double* x, int xs, double fu) {
+#ifndef DLP_BLOCK_BRANCH
+        // s takes a selected +0.0 for ground-truth entries (no per-entry
+        // branch, so the block's terms overlap); w0 / w1 are updated in one
+        // rarely taken branch per block, in entry order
+        double wv[B], xv[B], pv[B];
+        bool any = false;
+#pragma unroll
+        for (int j = 0; j < B; j++) {
+            wv[j] = w[j];
+            xv[j] = x[j * xs];
+        }
+#pragma unroll
+        for (int j = 0; j < B; j++) {
+            const bool gt = is_boxed(xv[j]);
+            any |= gt;
+            const double p = __dmul_rn(__dsub_rn(xv[j], fu), wv[j]);
+            pv[j] = gt ? 0.0 : p;
+        }
+#pragma unroll
+        for (int j = 0; j < B; j++) {
+            w_all = __dadd_rn(w_all, wv[j]);
+            s = __dadd_rn(s, pv[j]);
+        }
+        if (any) {
+#pragma unroll
+            for (int j = 0; j < B; j++)
+                if (is_boxed(xv[j])) {
+                    if (__double2loint(xv[j]) & 1)
+                        w1 = __dadd_rn(w1, wv[j]);
+                    else
+                        w0 = __dadd_rn(w0, wv[j]);
+                }
+        }
+#else
 #pragma unroll
         for (int j = 0; j < B; j++) add_boxed(w[j], x[j * xs], fu);
+#endif
     }
     // returns |fn - fu| or -1 for the isolated sentinel (value 0.5)
     __device__ inline double finish(double fu, double* out_val) const {

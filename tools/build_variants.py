@@ -15,6 +15,8 @@ VARIANTS = {
     "w64": ["DLP_WIN=64"],
     "sel": ["DLP_SUMS_SELECT"],
     "pred": ["DLP_SUMS_PRED"],
+    "blkbr": ["DLP_BLOCK_BRANCH"],
+    "blk8": ["DLP_ACC_UNROLL=8"],
     "lp2": ["DLP_LONG_PER=2"],
     "u2": ["DLP_ACC_UNROLL=2"],
     "u8": ["DLP_ACC_UNROLL=8"],
