@@ -57,7 +57,7 @@ constexpr int kLpThreads = 256;
 #define DLP_WIN 32
 #endif
 #ifndef DLP_HUB_WIN
-#define DLP_HUB_WIN 256
+#define DLP_HUB_WIN 128
 #endif
 #ifndef DLP_LP_MINB
 #define DLP_LP_MINB 3

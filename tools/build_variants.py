@@ -16,6 +16,8 @@ VARIANTS = {
     "sel": ["DLP_SUMS_SELECT"],
     "pred": ["DLP_SUMS_PRED"],
     "blkbr": ["DLP_BLOCK_BRANCH"],
+    "hw128": ["DLP_HUB_WIN=128"],
+    "hw64": ["DLP_HUB_WIN=64"],
     "blk8": ["DLP_ACC_UNROLL=8"],
     "lp2": ["DLP_LONG_PER=2"],
     "u2": ["DLP_ACC_UNROLL=2"],
