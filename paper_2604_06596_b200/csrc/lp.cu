@@ -164,8 +164,13 @@ __device__ inline void cp_async8(double* dst, const double* src, unsigned long l
 }
 __device__ inline void cp_async16(double* dst, const double* src, unsigned long long pol) {
     unsigned int d = (unsigned int)__cvta_generic_to_shared(dst);
+#ifdef DLP_CP16_CA  // variant: keep the label rows in L1 as well
+    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "l"(pol)
+                 : "memory");
+#else
     asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "l"(pol)
                  : "memory");
+#endif
 }
 __device__ inline void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
@@ -1077,6 +1082,10 @@ __device__ void cta_hub_row(const LPParams& P, const RoundCtx& R, ClaimCtx& K, B
     __syncthreads();
 }
 
+// Grid barrier of the persistent kernel: one arrival counter (a two-level
+// variant with 16 group counters measured 1% slower at 444 CTAs).
+__device__ inline void gsync(LPCtl* ctl, unsigned int& target) { grid_sync(&ctl->bar, target); }
+
 __global__ void __launch_bounds__(kLpThreads, DLP_LP_MINB) k_lp_fused(LPParams P) {
     extern __shared__ double smem_dyn[];
     __shared__ ColState S;
@@ -1167,7 +1176,7 @@ __global__ void __launch_bounds__(kLpThreads, DLP_LP_MINB) k_lp_fused(LPParams P
         if (blockIdx.x == 0 && !resume)
             for (int c = 0; c < C; c++) ctl->elig_count[c] = n_el;
     }
-    grid_sync(&ctl->bar, target);
+    gsync(ctl, target);
     if (tid == 0) {
         if (P.action_mode)
             decide_actions_act(S, P, nullptr, nullptr, 1);
@@ -1284,7 +1293,7 @@ __global__ void __launch_bounds__(kLpThreads, DLP_LP_MINB) k_lp_fused(LPParams P
             if (B.urows) atomicAdd(&slot->urows, B.urows);
             if (B.uent) atomicAdd(&slot->uentries, B.uent);
         }
-        grid_sync(&ctl->bar, target);
+        gsync(ctl, target);
         if (ctl->trace && gtid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_p1));
 #ifdef DLP_PROF
         if (ctl->prof && (tid & 31) == 0) {
@@ -1403,7 +1412,7 @@ __global__ void __launch_bounds__(kLpThreads, DLP_LP_MINB) k_lp_fused(LPParams P
             nx->uentries = 0;
             for (int j = 0; j < 3; j++) nx->grab[j] = nx->cnt[j] = 0;
         }
-        grid_sync(&ctl->bar, target);
+        gsync(ctl, target);
         // controller: stage the slot's per-column results in shared memory
         // (parallel loads), then one thread replays the state machines
         {
@@ -1446,7 +1455,7 @@ __global__ void __launch_bounds__(kLpThreads, DLP_LP_MINB) k_lp_fused(LPParams P
     }
     if (P.action_mode && !P.cleanup) {
         // hand the lists and per-column phase results to the host
-        grid_sync(&ctl->bar, target);  // every CTA has read ctl before it is rewritten
+        gsync(ctl, target);  // every CTA has read ctl before it is rewritten
         if (gtid == 0) {
             for (int c = 0; c < C; c++) {
                 ctl->has_fr[c] = S.has_frontier[c];
@@ -1527,6 +1536,8 @@ void lp_setup(Engine& E) {
     E.lp_smem = std::max(E.lp_smem, (size_t)4 * kPCSlots * pc_slot_bytes(E.ncol));
 #endif
     DLP_CUDA_TRY(cudaFuncSetAttribute(k_lp_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)E.lp_smem));
+    if (const char* v = getenv("DLP_CARVEOUT"))  // shared-memory share of L1 (percent), tuning
+        DLP_CUDA_TRY(cudaFuncSetAttribute(k_lp_fused, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(v)));
     int occ = 0;
     DLP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_lp_fused, kLpThreads, E.lp_smem));
     if (occ < 1) occ = 1;

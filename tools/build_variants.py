@@ -16,7 +16,7 @@ VARIANTS = {
     "sel": ["DLP_SUMS_SELECT"],
     "pred": ["DLP_SUMS_PRED"],
     "blkbr": ["DLP_BLOCK_BRANCH"],
-    "hw128": ["DLP_HUB_WIN=128"],
+    "ca16": ["DLP_CP16_CA"],
     "hw64": ["DLP_HUB_WIN=64"],
     "blk8": ["DLP_ACC_UNROLL=8"],
     "lp2": ["DLP_LONG_PER=2"],
