@@ -55,6 +55,55 @@ def test_torch_collective_gloo_world2():
         assert imax == [10, 5] and isum == [3, 200] and dmax == [0.25, 0.0]
 
 
+def _rows_gather_worker(rank, world, port, q):
+    """The row partition's all-gather (abi.cu rows_exchange): each rank writes
+    its rows (vertex, masks, label bit patterns) into its own segment of an
+    int64 vector; the sum-reduction must return every rank's words exactly."""
+    sys.path.insert(0, os.path.dirname(HERE))
+    import torch.distributed as dist
+
+    from paper_2604_06596_b200.sharded import torch_collective
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    coll = torch_collective()
+    C = 3
+    rng = np.random.default_rng(rank)
+    cnt = np.zeros(world, np.int64)
+    mine = 5 + rank
+    cnt[rank] = mine
+    coll(np.zeros(1, np.int64), cnt, np.zeros(1))
+    off = int(cnt[:rank].sum())
+    vals = rng.random((mine, C))
+    vals[0, 0] = -0.0
+    vals[1, 1] = np.frombuffer(np.uint64(0x7FF4000000000001).tobytes(), np.float64)[0]  # boxed class 1
+    buf = np.zeros((int(cnt.sum()), 3 + C), np.int64)
+    buf[off:off + mine, 0] = np.arange(mine) * world + rank
+    buf[off:off + mine, 1] = 0b101
+    buf[off:off + mine, 2] = 0b100
+    buf[off:off + mine, 3:] = vals.view(np.int64)
+    flat = buf.ravel().copy()
+    coll(np.zeros(1, np.int64), flat, np.zeros(1))
+    q.put((rank, cnt.tolist(), flat.tolist(), vals.view(np.int64).tolist()))
+    dist.destroy_process_group()
+
+
+def test_rows_allgather_exact_gloo_world2():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_rows_gather_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    out = sorted(q.get(timeout=120) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+    (r0, cnt0, flat0, v0), (r1, cnt1, flat1, v1) = out
+    assert cnt0 == cnt1 == [5, 6] and flat0 == flat1
+    g = np.array(flat0, np.int64).reshape(11, 6)
+    assert g[:5, 3:].tolist() == v0 and g[5:, 3:].tolist() == v1  # label bit patterns survive exactly
+    assert g[:5, 0].tolist() == [0, 2, 4, 6, 8] and g[5:, 0].tolist() == [1, 3, 5, 7, 9, 11]
+
+
 def test_in_process_collective_threads():
     import threading
 
