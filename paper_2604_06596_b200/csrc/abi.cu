@@ -169,8 +169,11 @@ BatchDev stage_batch(Engine& E, const HostBatch& b, int slot = 0, cudaStream_t s
     off[6] = tot;
     // both staging slots grow together, with a floor, so the ingestion
     // pipeline never allocates pinned memory (or its copy stream) mid-stream
-    const size_t want = std::max(tot + 256, (size_t)32 << 20);
-    if (hs.n < tot + 256) {
+    const size_t need = tot + 256;
+    static const size_t floor_b = getenv("DLP_STAGE_FLOOR_MB") ? (size_t)atol(getenv("DLP_STAGE_FLOOR_MB")) << 20
+                                                                 : (size_t)32 << 20;
+    const size_t want = std::max(need + need / 2, floor_b);
+    if (hs.n < need || ds.n < need) {  // pinned and device slots grow by different rules
         E.h_stage.reserve(want);
         E.h_stage2.reserve(want);
         E.d_stage.reserve(want, 0, E.st);

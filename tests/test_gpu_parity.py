@@ -216,6 +216,19 @@ def test_row_class_paths(gpu_device, ncls, long_row, hub_row):
     assert r.returncode == 0, r.stdout + r.stderr
 
 
+def test_ingestion_pipeline_staging_growth(gpu_device):
+    """Staging slots outgrown between pipelined batches (floor 0): bit-identical."""
+    import os
+    import subprocess
+    import sys
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    env = dict(os.environ, DLP_STAGE_FLOOR_MB="0")
+    r = subprocess.run([sys.executable, os.path.join(here, "_staging_check.py")], env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
 def test_ingestion_pipeline_identical_and_atomic(gpu_device):
     """apply_batch(..., next_batch=) validates and stages the next batch while
     the current one runs: identical reports and labels; a bad next batch is
