@@ -102,7 +102,7 @@ struct LPParams {
     double* X;  // canonical labels [v*C + c]
     double* Y;  // compact staging: [i*C + c] for work item i of the round
     unsigned int* eligm;
-    unsigned int* emask_store;
+    unsigned int* emask_store;  // evaluated column mask per work item of the round
     unsigned int* fmask[2];
     int* flist[3][2];  // union frontier lists per row class (rotating)
     int* elist_c[3];   // eligible list split by row class (prologue)
@@ -411,7 +411,7 @@ __device__ void warp_tile(const LPParams& P, const RoundCtx& R, ClaimCtx& K, Blo
     unsigned int em = 0;
     if (lane < nrows) {
         em = m.em;
-        P.emask_store[m.u] = em;
+        P.emask_store[R.ybase + k0 + lane] = em;  // by work item: the commit reads it coalesced
         len = em ? m.len : 0;
         T.u[lane] = m.u;
         T.em[lane] = em;
@@ -695,7 +695,7 @@ __device__ void pc_produce_class(const LPParams& P, const RoundCtx& R, unsigned 
         long long st = 0;
         if (lane < nr) {
             em = m.em;
-            P.emask_store[m.u] = em;
+            P.emask_store[R.ybase + k + lane] = em;
             len = em ? m.len : 0;
             st = em ? m.st : 0;
         }
@@ -870,7 +870,7 @@ __device__ void cta_hub_row(const LPParams& P, const RoundCtx& R, ClaimCtx& K, B
     if (tid == 0) {
         int u = R.W[k];
         unsigned int em = P.itlp ? (R.CE & P.eligm[u]) : (((R.fm_cur[u] & R.FR) | R.CE) & P.eligm[u]);
-        P.emask_store[u] = em;
+        P.emask_store[R.ybase + k] = em;
         s_i[0] = u;
         s_u32[0] = em;
         s_u32[1] = 0;
@@ -1314,10 +1314,12 @@ __global__ void __launch_bounds__(kLpThreads, DLP_LP_MINB) k_lp_fused(LPParams P
             for (int h = 0; h < 2; h++) {
                 const long long i = i0 + h * gth;
                 uu[h] = -1;
-                if (i < nwork) uu[h] = i < n0c ? W0[i] : (i < n0c + n1c ? W1[i - n0c] : W2[i - n0c - n1c]);
+                ee[h] = 0u;
+                if (i < nwork) {
+                    uu[h] = i < n0c ? W0[i] : (i < n0c + n1c ? W1[i - n0c] : W2[i - n0c - n1c]);
+                    ee[h] = P.emask_store[i];  // coalesced, independent of the list lookup
+                }
             }
-#pragma unroll
-            for (int h = 0; h < 2; h++) ee[h] = uu[h] >= 0 ? P.emask_store[uu[h]] : 0u;
 #pragma unroll
             for (int h = 0; h < 2; h++) {
                 const long long i = i0 + h * gth;

@@ -6,6 +6,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2604_06596_b200 import build  # noqa: E402
 
 VARIANTS = {
+    "prev": [],  # the committed source (A/B against a working-tree change)
     "hubprof": ["DLP_HUBPROF"],
     "minb2": ["DLP_LP_MINB=2"],
     "minb2hp": ["DLP_LP_MINB=2", "DLP_HUBPROF"],
