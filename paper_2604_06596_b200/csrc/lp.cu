@@ -74,7 +74,7 @@ constexpr int kWin = DLP_WIN;   // row entries per warp window
 constexpr int kHubWin = DLP_HUB_WIN;  // row entries per CTA window (hub rows)
 constexpr int kLongRow = 96;    // rows longer than this are warp tiles of their own
 #ifndef DLP_HUB_ROW_DEFAULT
-#define DLP_HUB_ROW_DEFAULT 384
+#define DLP_HUB_ROW_DEFAULT 512
 #endif
 constexpr int kHubRow = DLP_HUB_ROW_DEFAULT;  // rows longer than this are evaluated by a whole CTA
 constexpr int kScanRatio = 64;  // rounds with >= n/64 rows expand by atomicOr + compaction
