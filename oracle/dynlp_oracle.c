@@ -773,12 +773,13 @@ static void reachable(orc_engine* e, uint8_t* reached) {
 /* _Propagator.step / expand (engine.py:253-288) */
 static int64_t prop_step(orc_engine* e, const orc_config* cfg, const int8_t* gtc, double* f,
                          uint8_t* elig, const int64_t* frontier, int64_t nf, int64_t* next,
-                         uint8_t* flags, double* max_change, int64_t* warnings, int64_t* edges) {
+                         uint8_t* flags, double* max_change, int64_t* warnings, int64_t* edges,
+                         int32_t threads) {
     double* vals = (double*)xrealloc(NULL, sizeof(double) * (nf + 1));
     double* deltas = (double*)xrealloc(NULL, sizeof(double) * (nf + 1));
     if (cfg->mode == 0) {
         orc_jacobi_step(e->indptr, e->indices, e->weights, gtc, f, frontier, nf, vals, deltas,
-                        e->threads);
+                        threads);
         for (int64_t i = 0; i < nf; i++) f[frontier[i]] = vals[i];
     } else {
         orc_gauss_seidel_step(e->indptr, e->indices, e->weights, gtc, f, frontier, nf, deltas);
@@ -812,6 +813,92 @@ static int64_t prop_step(orc_engine* e, const orc_config* cfg, const int8_t* gtc
     return m;
 }
 
+/* One label column of apply_batch (engine.py:345-405 after the shared
+ * structure / tau / intra-batch components / reachability): init, pin,
+ * frontier rounds and certify sweeps.  Writes only column c's labels and its
+ * own scratch, so columns may run concurrently. */
+static void run_column(orc_engine* e, const orc_config* cfg, int c, const uint8_t* mark,
+                       const uint8_t* reached, int64_t isolated, int64_t unreach, int64_t max_iter,
+                       int do_init, int32_t threads, orc_report* rep) {
+    int64_t n = e->n_slots;
+    int8_t* gtc = (int8_t*)xrealloc(NULL, n + 1);
+    uint8_t* elig = (uint8_t*)xrealloc(NULL, n + 1);
+    uint8_t* flags = (uint8_t*)calloc(n + 1, 1);
+    int64_t* frontier = (int64_t*)xrealloc(NULL, sizeof(int64_t) * (n + 1));
+    int64_t* next = (int64_t*)xrealloc(NULL, sizeof(int64_t) * (n + 1));
+    int64_t* ids = (int64_t*)xrealloc(NULL, sizeof(int64_t) * (n + 1));
+    double* f = e->f + c * e->cap;
+    column_gt(e, c, gtc);
+    if (do_init) init_components(e, c, gtc);
+    for (int64_t v = 0; v < n; v++) /* pin unreachable (engine.py:353-360) */
+        if (e->alive[v] && e->gt[v] == -1 && !reached[v]) f[v] = 0.5;
+    memcpy(elig, e->last_elig, n);
+    /* restrict(seeds) (engine.py:246-251, 364-367): sorted, eligible */
+    int64_t nf = 0;
+    for (int64_t v = 0; v < n; v++)
+        if (mark[v] && elig[v]) frontier[nf++] = v;
+    int64_t iterations = 0, updates = 0, warnings = 0, edges = 0, certs = 0;
+    double max_change = 0.0;
+    int converged = 1;
+    for (;;) {
+        if (cfg->mode == 0) {
+            int64_t it, upd, warn;
+            double mc;
+            nf = jacobi_run_impl(e->indptr, e->indices, e->weights, gtc, f, n, frontier, nf, elig,
+                                 cfg->delta, max_iter - iterations, threads, &it, &upd, &mc, &warn,
+                                 next, &edges);
+            int64_t* tmp = frontier;
+            frontier = next;
+            next = tmp;
+            iterations += it;
+            updates += upd;
+            warnings += warn;
+            if (it) max_change = mc;
+        } else {
+            while (nf && iterations < max_iter) {
+                updates += nf;
+                nf = prop_step(e, cfg, gtc, f, elig, frontier, nf, next, flags, &max_change,
+                               &warnings, &edges, threads);
+                int64_t* tmp = frontier;
+                frontier = next;
+                next = tmp;
+                iterations++;
+            }
+        }
+        if (nf || iterations >= max_iter) {
+            converged = nf == 0;
+            if (!converged) break;
+        }
+        /* certify_round (engine.py:290-301) */
+        int64_t ni = 0;
+        for (int64_t v = 0; v < n; v++)
+            if (elig[v]) ids[ni++] = v;
+        if (ni == 0) break;
+        double mc;
+        nf = prop_step(e, cfg, gtc, f, elig, ids, ni, frontier, flags, &mc, &warnings, &edges, threads);
+        certs++;
+        iterations++;
+        updates += ni;
+        max_change = mc;
+        if (mc <= cfg->delta) break;
+    }
+    rep->iterations = iterations;
+    rep->updates = updates;
+    rep->max_change = max_change;
+    rep->converged = converged;
+    rep->isolated_pinned = isolated;
+    rep->unreachable_pinned = unreach;
+    rep->warnings = warnings + isolated + unreach;
+    rep->edges_traversed = edges;
+    rep->certify_sweeps = certs;
+    free(gtc);
+    free(elig);
+    free(flags);
+    free(frontier);
+    free(next);
+    free(ids);
+}
+
 static int apply_batch_impl(orc_engine* e, const orc_config* cfg, const orc_batch* b,
                             orc_report* reps, int structure_only) {
     double t0 = now_ms();
@@ -840,7 +927,6 @@ static int apply_batch_impl(orc_engine* e, const orc_config* cfg, const orc_batc
     int64_t n = e->n_slots;
     e->last_tau = resolve_tau(e, cfg);
     e->intra_n = 0;
-    int8_t* gtc = (int8_t*)xrealloc(NULL, n + 1);
     int do_init = cfg->component_init && b->n_ins > 0;
     if (do_init) intra_components(e, b, e->last_tau);
     build_csr(e);
@@ -859,87 +945,19 @@ static int apply_batch_impl(orc_engine* e, const orc_config* cfg, const orc_batc
     }
     int64_t max_iter = cfg->max_iterations > 0 ? cfg->max_iterations
                                                 : (10 * e->num_alive > 1 ? 10 * e->num_alive : 1);
-    uint8_t* elig = (uint8_t*)xrealloc(NULL, n + 1);
-    uint8_t* flags = (uint8_t*)calloc(n + 1, 1);
-    int64_t* frontier = (int64_t*)xrealloc(NULL, sizeof(int64_t) * (n + 1));
-    int64_t* next = (int64_t*)xrealloc(NULL, sizeof(int64_t) * (n + 1));
-    int64_t* ids = (int64_t*)xrealloc(NULL, sizeof(int64_t) * (n + 1));
-    for (int c = 0; c < ncol; c++) {
-        double* f = e->f + c * e->cap;
-        column_gt(e, c, gtc);
-        if (do_init) init_components(e, c, gtc);
-        for (int64_t v = 0; v < n; v++) /* pin unreachable (engine.py:353-360) */
-            if (e->alive[v] && e->gt[v] == -1 && !reached[v]) f[v] = 0.5;
-        memcpy(elig, e->last_elig, n);
-        /* restrict(seeds) (engine.py:246-251, 364-367): sorted, eligible */
-        int64_t nf = 0;
-        for (int64_t v = 0; v < n; v++)
-            if (mark[v] && elig[v]) frontier[nf++] = v;
-        int64_t iterations = 0, updates = 0, warnings = 0, edges = 0, certs = 0;
-        double max_change = 0.0;
-        int converged = 1;
-        for (;;) {
-            if (cfg->mode == 0) {
-                int64_t it, upd, warn;
-                double mc;
-                nf = jacobi_run_impl(e->indptr, e->indices, e->weights, gtc, f, n, frontier, nf,
-                                     elig, cfg->delta, max_iter - iterations, e->threads, &it,
-                                     &upd, &mc, &warn, next, &edges);
-                int64_t* tmp = frontier;
-                frontier = next;
-                next = tmp;
-                iterations += it;
-                updates += upd;
-                warnings += warn;
-                if (it) max_change = mc;
-            } else {
-                while (nf && iterations < max_iter) {
-                    updates += nf;
-                    nf = prop_step(e, cfg, gtc, f, elig, frontier, nf, next, flags, &max_change,
-                                   &warnings, &edges);
-                    int64_t* tmp = frontier;
-                    frontier = next;
-                    next = tmp;
-                    iterations++;
-                }
-            }
-            if (nf || iterations >= max_iter) {
-                converged = nf == 0;
-                if (!converged) break;
-            }
-            /* certify_round (engine.py:290-301) */
-            int64_t ni = 0;
-            for (int64_t v = 0; v < n; v++)
-                if (elig[v]) ids[ni++] = v;
-            if (ni == 0) break;
-            double mc;
-            nf = prop_step(e, cfg, gtc, f, elig, ids, ni, frontier, flags, &mc, &warnings, &edges);
-            certs++;
-            iterations++;
-            updates += ni;
-            max_change = mc;
-            if (mc <= cfg->delta) break;
-        }
-        reps[c].iterations = iterations;
-        reps[c].updates = updates;
-        reps[c].max_change = max_change;
-        reps[c].converged = converged;
-        reps[c].isolated_pinned = isolated;
-        reps[c].unreachable_pinned = unreach;
-        reps[c].warnings = warnings + isolated + unreach;
-        reps[c].edges_traversed = edges;
-        reps[c].certify_sweeps = certs;
-    }
+    /* The C one-vs-rest columns are independent reference runs sharing the
+     * structure: with threads > 1 and several columns they run concurrently
+     * (one column per thread, each column's own rounds serial), otherwise
+     * one after the other with the kernel's own threading. */
+    int col_par = ncol > 1 && e->threads > 1;
+    int inner = col_par ? 1 : e->threads;
+#pragma omp parallel for schedule(dynamic, 1) num_threads(col_par ? (e->threads < ncol ? e->threads : ncol) : 1)
+    for (int c = 0; c < ncol; c++)
+        run_column(e, cfg, c, mark, reached, isolated, unreach, max_iter, do_init, inner, &reps[c]);
     double dt = now_ms() - t0;
     for (int c = 0; c < ncol; c++) reps[c].wall_time_ms = dt;
     free(mark);
-    free(gtc);
     free(reached);
-    free(elig);
-    free(flags);
-    free(frontier);
-    free(next);
-    free(ids);
     return 0;
 }
 

@@ -247,6 +247,7 @@ void stage_next(Engine& E, const dlp_batch* nb) {
     s.nd = nb->n_del;
     const void* p[6] = {nb->insert_ids, nb->insert_gt, nb->edge_owner, nb->edge_other, nb->edge_w, nb->deletes};
     for (int i = 0; i < 6; i++) s.ptrs[i] = p[i];
+    s.dels.assign((const long long*)nb->deletes, (const long long*)nb->deletes + nb->n_del);
     HostBatch hb{nb->t, nb->n_ins, nb->n_edges, nb->n_del, (const long long*)nb->insert_ids,
                  (const long long*)nb->edge_owner, (const long long*)nb->edge_other, (const long long*)nb->deletes,
                  (const signed char*)nb->insert_gt, nb->edge_w};
@@ -507,6 +508,12 @@ int run_batch(dlp_engine* h, const dlp_config* cfg, const dlp_batch* batch, bool
         if (reps)
             for (int c = 0; c < E.ncol; c++) reps[c].wall_time_ms = ms;
     };
+    // The ingestion pipeline's staged batch is only usable by the very next
+    // host batch with the same arrays; any other call (device batches, a
+    // different or empty batch) invalidates it, since it was validated
+    // against a host mirror that call may advance.
+    const bool use_staged = !device_ptrs && staged_matches(E, batch);
+    if (!use_staged) E.staged.valid = false;
     if (batch->n_ins == 0 && batch->n_del == 0 && kind != KIND_ITLP) {  // engine.py:338-340
         finish_time();
         return DLP_OK;
@@ -545,12 +552,11 @@ int run_batch(dlp_engine* h, const dlp_config* cfg, const dlp_batch* batch, bool
             hb.w = hv_w.data();
             hb.dels = hv_dels.data();
         }
-        const bool use_staged = !device_ptrs && staged_matches(E, batch);
         if (use_staged) {  // validated and copied during the previous batch
             E.staged.valid = false;
             if (E.staged.rc) return fail(E, E.staged.rc, "%s", E.staged.err.c_str());
+            hb.dels = E.staged.dels.data();  // the copy the device applies (mirror update below)
         } else if (!(device_ptrs && trusted)) {
-            E.staged.valid = false;
             int rc = validate_batch(E, hb);
             if (rc) return rc;
         }
@@ -698,6 +704,20 @@ int run_batch(dlp_engine* h, const dlp_config* cfg, const dlp_batch* batch, bool
     }
 }
 
+// Label read-out (LabelState.f, labels.py:21): column c of vertex v to
+// out[c * n + v]; a boxed ground-truth word becomes its class as 0.0 / 1.0
+// (the reference pins f = class, labels.py:37-49).  Any other NaN is an
+// unlabeled vertex's label and is returned as is.
+__global__ void k_labels_out(const double* X, long long n, int C, double* out) {
+    const long long tot = n * C;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < tot; i += (long long)gridDim.x * blockDim.x) {
+        const long long c = i / n, v = i - c * n;
+        const double x = X[v * C + c];
+        const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+        out[i] = (b & ~1ULL) == kBoxBase ? (double)(b & 1ULL) : x;
+    }
+}
+
 }  // namespace
 
 extern "C" {
@@ -725,6 +745,10 @@ int dlp_create(const dlp_config* cfg, int device, dlp_engine** out) {
         E.host_trace = getenv("DLP_HOST_TRACE") != nullptr;
         E.num_classes = cfg && cfg->num_classes > 2 ? cfg->num_classes : 2;
         E.ncol = E.num_classes > 2 ? E.num_classes : 1;
+        if (E.ncol > kMaxCols) {  // before anything is allocated
+            delete h;
+            return DLP_EVALIDATION;
+        }
         DLP_CUDA_TRY(cudaStreamCreateWithFlags(&E.st, cudaStreamNonBlocking));
         {  // keep freed stream-ordered allocations cached in the device pool
             cudaMemPool_t mp;
@@ -734,10 +758,6 @@ int dlp_create(const dlp_config* cfg, int device, dlp_engine** out) {
         }
         DLP_CUDA_TRY(cudaMalloc(&E.ds, sizeof(DevState)));
         DLP_CUDA_TRY(cudaMemset(E.ds, 0, sizeof(DevState)));
-        if (E.ncol > kMaxCols) {
-            delete h;
-            return DLP_EVALIDATION;
-        }
         DLP_CUDA_TRY(cudaMalloc(&E.ctl, sizeof(LPCtl)));
         DLP_CUDA_TRY(cudaMemset(E.ctl, 0, sizeof(LPCtl)));
         E.h_ds.reserve(1);
@@ -846,7 +866,7 @@ int dlp_destroy(dlp_engine* h) {
                              &E.flag_i, &E.pos_i, &E.m_lo, &E.m_hi, &E.mlo_at, &E.mhi_at, &E.lpar, &E.comp,
                              &E.comp_sorted_i, &E.root_flag, &E.root_rank, &E.root_tmp, &E.log_u, &E.rx_u};
     for (auto* a : i32s) a->release();
-    DevArray<double>* f64s[] = {&E.f[0], &E.f[1], &E.wgt, &E.wgt_sp, &E.log_w, &E.log_w2, &E.m_w, &E.ew_lo, &E.ew_hi,
+    DevArray<double>* f64s[] = {&E.f[0], &E.f[1], &E.readout, &E.wgt, &E.wgt_sp, &E.log_w, &E.log_w2, &E.m_w, &E.ew_lo, &E.ew_hi,
                                 &E.mw_at, &E.per0, &E.per1, &E.cinit, &E.tau_scratch, &E.rx_val};
     for (auto* a : f64s) a->release();
     DevArray<unsigned int>* u32s[] = {&E.eligm, &E.emask_store, &E.fmask[0], &E.fmask[1], &E.log_em, &E.log_chg,
@@ -900,33 +920,18 @@ int dlp_read_labels(dlp_engine* h, double* f, int8_t* gt, int64_t n) {
     if (n != E.n_slots) return fail(E, DLP_EVALIDATION, "read_labels: n=%lld but num_slots=%lld", (long long)n, E.n_slots);
     try {
         DLP_CUDA_TRY(cudaSetDevice(E.device));
-        std::vector<double> buf;
-        if (f && n) {
-            if (E.ncol == 1) {
-                DLP_CUDA_TRY(cudaMemcpyAsync(f, E.f[0].p, n * sizeof(double), cudaMemcpyDeviceToHost, E.st));
-            } else {
-                buf.resize((size_t)n * E.ncol);
-                DLP_CUDA_TRY(cudaMemcpyAsync(buf.data(), E.f[0].p, buf.size() * sizeof(double), cudaMemcpyDeviceToHost,
-                                             E.st));
-            }
+        if (f && n) {  // unbox + column-major transpose on the device, one D2H copy
+            E.readout.reserve((size_t)n * E.ncol, 0, E.st);
+            k_labels_out<<<blocks_for((long long)n * E.ncol), kBlock, 0, E.st>>>(E.f[0].p, n, E.ncol, E.readout.p);
+            DLP_CUDA_TRY(cudaGetLastError());
+            DLP_CUDA_TRY(cudaMemcpyAsync(f, E.readout.p, (size_t)n * E.ncol * sizeof(double), cudaMemcpyDeviceToHost,
+                                         E.st));
         }
         if (gt && n) DLP_CUDA_TRY(cudaMemcpyAsync(gt, E.gt.p, n, cudaMemcpyDeviceToHost, E.st));
         DLP_CUDA_TRY(cudaStreamSynchronize(E.st));
-        if (f && E.ncol > 1)
-            for (long long v = 0; v < n; v++)
-                for (int c = 0; c < E.ncol; c++) f[(size_t)c * n + v] = buf[(size_t)v * E.ncol + c];
     } catch (const CudaFailure& e) {
         return cuda_fail(h, e);
     }
-    if (f)
-        for (long long i = 0; i < (long long)E.ncol * n; i++) {
-            double x = f[i];
-            if (x != x) {
-                unsigned long long b;
-                memcpy(&b, &x, 8);
-                f[i] = (double)(b & 1);
-            }
-        }
     return DLP_OK;
 }
 
@@ -941,6 +946,7 @@ int dlp_write_labels(dlp_engine* h, const double* f, int64_t n) {
         for (int c = 0; c < E.ncol; c++)
             for (long long v = 0; v < n; v++) {
                 double x = f[(size_t)c * n + v];
+                if (x != x) x = std::nan("");  // a caller NaN stays an unlabeled NaN, never a box
                 if (g[v] >= 0) x = box_class(E.ncol == 1 ? g[v] : (g[v] == c ? 1 : 0));
                 buf[(size_t)v * E.ncol + c] = x;
             }

@@ -37,7 +37,13 @@ __host__ __device__ inline double box_class(int c) {
     x.u = kBoxBase | (unsigned long long)(c & 1);
     return x.d;
 }
-__device__ inline bool is_boxed(double x) { return x != x; }
+constexpr int kBoxHi = 0x7FF40000;  // high word of a boxed ground-truth label
+// Exact box test on the high word (one integer compare, the cost of the NaN
+// test it replaces): a NaN an unlabeled vertex reaches through non-finite
+// weights (the reference keeps such a NaN, _csr.pyx:52-56) is not a box, so
+// its neighbours treat it as an unlabeled NaN label exactly as the reference
+// does.  Arithmetic never produces this signalling-NaN pattern.
+__device__ inline bool is_boxed(double x) { return __double2hiint(x) == kBoxHi; }
 __device__ inline int boxed_class(double x) { return (int)(__double_as_longlong(x) & 1); }
 __device__ inline double unbox(double x) { return is_boxed(x) ? (double)boxed_class(x) : x; }
 

@@ -195,6 +195,7 @@ struct Engine {
     DevArray<long long> row_start;
     DevArray<int> row_len, row_up, row_cap, parent, cnt_up, cnt_dn, grp_start;
     DevArray<double> f[2];
+    DevArray<double> readout;  // dlp_read_labels: unboxed column-major labels
     DevArray<unsigned int> eligm, emask_store, fmask[2];
     DevArray<int> ulist[2], llist[2], hlist[2], elist_s, elist_l, elist_h, f0, elist, purge_list, touched;
     // adjacency pool ------------------------------------------------------

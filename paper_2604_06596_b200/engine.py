@@ -133,6 +133,8 @@ class DynamicGraph:
         cfg = EngineConfig()._c(self.num_classes)
         h = C.c_void_p()
         rc = self._lib.dlp_create(C.byref(cfg), self.device, C.byref(h))
+        if rc == 3:
+            raise ValidationError(f"num_classes must be <= 16 (got {self.num_classes})")
         if rc != 0 or not h.value:
             raise CudaError(f"dlp_create failed on device {device} (rc={rc}); a B200 (sm_100a) is required")
         self._h = h

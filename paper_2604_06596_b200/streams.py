@@ -107,6 +107,30 @@ def knn_graph_torch(x: np.ndarray, k: int, device: str = "cuda", block: int = 81
     return _symmetrize(np.concatenate(srcs), np.concatenate(dsts), np.concatenate(sims), n)
 
 
+def knn_graph_torch64(x: np.ndarray, k: int, device: str = "cuda", block: int = 2048) -> EdgeList:
+    """Cosine k-NN in fp64 through torch (GPU GEMM + top-k), the bench's
+    synthetic-stream generator.  Input generation only, shared by both bench
+    arms so that the reference arm never loads this repo's CUDA library: the
+    edge set equals the exact numpy selection (knn_graph_exact) except on
+    sub-ulp near-ties, whose order follows the GEMM's summation order."""
+    import torch
+
+    n = x.shape[0]
+    xt = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).to(device)
+    xt = xt / torch.linalg.vector_norm(xt, dim=1, keepdim=True)
+    srcs, dsts, sims = [], [], []
+    for s in range(0, n, block):
+        e = min(n, s + block)
+        sim = xt[s:e] @ xt.T
+        sim[torch.arange(e - s, device=device), torch.arange(s, e, device=device)] = -float("inf")
+        val, idx = torch.topk(sim, k, dim=1, sorted=True)
+        srcs.append(np.repeat(np.arange(s, e, dtype=np.int64), k))
+        dsts.append(idx.reshape(-1).cpu().numpy().astype(np.int64))
+        sims.append(val.reshape(-1).cpu().numpy())
+        del sim
+    return _symmetrize(np.concatenate(srcs), np.concatenate(dsts), np.concatenate(sims), n)
+
+
 def erdos_renyi_edges(n: int, avg_degree: float, seed: int, low=0.1, high=1.0) -> EdgeList:
     rng = np.random.default_rng(seed)
     m = int(rng.binomial(n * (n - 1) // 2, min(1.0, avg_degree / max(1, n - 1))))

@@ -259,3 +259,61 @@ def test_ingestion_pipeline_identical_and_atomic(gpu_device):
     assert l3.F.tobytes() == F_before.tobytes()
     for g in (g1, g2, g3):
         g.close()
+
+
+def test_staged_batch_invalidated_by_device_batch(gpu_device):
+    """A batch staged by the ingestion pipeline was validated against the host
+    mirror of its time; a device batch applied in between must invalidate it,
+    so the stale batch is re-validated and rejected (graph.py:267-277)."""
+    import torch
+
+    from paper_2604_06596_b200.engine import EngineConfig, apply_batch
+
+    g, lab = _engine()
+    cfg = EngineConfig(delta=1e-6)
+    b1 = BatchUpdate.from_records([(0, [], 1), (1, [(1, 0, 1.0)], None), (2, [(2, 1, 0.5)], 0)])
+    b2 = BatchUpdate.from_records([(3, [(3, 2, 1.0)], None), (4, [(4, 3, 1.0)], None)], t=2)
+    apply_batch(g, lab, b1, cfg, next_batch=b2)
+    ids = torch.tensor([3], dtype=torch.int64, device="cuda")
+    dev = dict(t=1, n_ins=1, n_edges=1, n_del=0, insert_ids=ids,
+               insert_gt=torch.tensor([-1], dtype=torch.int8, device="cuda"),
+               edge_owner=torch.tensor([0], dtype=torch.int64, device="cuda"),
+               edge_other=torch.tensor([2], dtype=torch.int64, device="cuda"),
+               edge_w=torch.tensor([1.0], dtype=torch.float64, device="cuda"),
+               deletes=torch.empty(0, dtype=torch.int64, device="cuda"))
+    g.apply_device(dev, cfg, trusted=True)
+    assert g.num_slots == 4
+    with pytest.raises(ValidationError, match="insert ids must be the contiguous block 4..5"):
+        apply_batch(g, lab, b2, cfg)
+    assert g.num_slots == 4
+    g.close()
+
+
+def test_nonfinite_weights_nan_labels_like_oracle(gpu_device):
+    """An infinite edge weight drives unlabeled labels to NaN (the reference
+    keeps NaN: _csr.pyx:52-56 clamps only ordered values).  Such a NaN is an
+    unlabeled label, never a boxed ground-truth word: neighbours propagate it
+    exactly like the oracle does."""
+    from paper_2604_06596_b200.engine import EngineConfig, apply_batch
+
+    recs = [(0, [], 1), (1, [(1, 0, 1.0)], None), (2, [(2, 1, float("inf"))], None),
+            (3, [(3, 2, 1.0)], None), (4, [(4, 3, 2.0)], None), (5, [(5, 0, 1.0)], 0)]
+    b = BatchUpdate.from_records(recs)
+    g, lab = _engine()
+    orc = OracleEngine(2)
+    cfg = EngineConfig(delta=1e-6, max_iterations=40)
+    lab, rep = apply_batch(g, lab, b, cfg)
+    orep = orc.apply_batch(b, delta=1e-6, max_iterations=40)
+    assert report_tuple(_reports(rep)[0]) == report_tuple(orep[0])
+    f, of = lab.f, orc.labels()[0][0]
+    assert np.isnan(of).any()
+    assert np.array_equal(np.isnan(f), np.isnan(of))
+    assert np.array_equal(f[~np.isnan(f)], of[~np.isnan(of)])
+    g.close()
+
+
+def test_too_many_classes_is_a_validation_error(gpu_device):
+    from paper_2604_06596_b200.engine import DynamicGraph
+
+    with pytest.raises(ValidationError, match="num_classes must be <= 16"):
+        DynamicGraph(0, num_classes=17)

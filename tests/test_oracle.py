@@ -119,3 +119,17 @@ def test_oracle_vs_live_reference_mixed_blobs(seed):
         (o,) = orc.apply_batch(b, delta=1e-5)
         assert report_tuple(o) == report_tuple(r) and o.max_change == r.max_change
         assert orc.labels()[0][0].tobytes() == lab.f[: g.num_slots].tobytes()
+
+
+def test_column_parallel_oracle_is_bitwise_serial():
+    """The oracle runs one-vs-rest columns concurrently when threads > 1
+    (the columns are independent reference runs): identical to serial."""
+    from test_long_stream import _stream
+
+    batches = _stream(n_boot=6, n_mixed=8, bs=300, classes=5, seed=3)
+    a, b = OracleEngine(5, threads=1), OracleEngine(5, threads=4)
+    for t, x in enumerate(batches):
+        ra, rb = a.apply_batch(x), b.apply_batch(x)
+        assert [(r.iterations, r.updates, r.max_change, r.edges_traversed) for r in ra] == \
+            [(r.iterations, r.updates, r.max_change, r.edges_traversed) for r in rb], t
+        assert a.labels()[0].tobytes() == b.labels()[0].tobytes(), t
