@@ -151,6 +151,14 @@ int dlp_num_slots(dlp_engine* e, int64_t* n_slots, int64_t* num_alive);
 int dlp_read_labels(dlp_engine* e, double* f, int8_t* gt, int64_t n);
 /* Overwrite f (CPU-baseline hand-off and tests); GT entries are ignored. */
 int dlp_write_labels(dlp_engine* e, const double* f, int64_t n);
+/* Closed-form harmonic labels of the current graph on the device (dense
+ * Cholesky of the free-vertex system, cuSOLVER): replaces
+ * baselines.harmonic_solve (dynlp/baselines.py:163-190, harmonic_dense
+ * :109-160); stlp=1 adds the short-circuit solve's both-classes check
+ * (stlp_reduce, :278-287; same solution).  f: C x n (column c at f + c*n);
+ * *unreachable = alive vertices with no path to a ground-truth vertex
+ * (pinned to 0.5).  3 when more than dense_cap vertices are free. */
+int dlp_harmonic_solve(dlp_engine* e, int stlp, int64_t dense_cap, double* f, int64_t n, int64_t* unreachable);
 int dlp_read_alive(dlp_engine* e, uint8_t* alive, int64_t n);
 /* eligible mask of the last batch (engine.py:361), before the loop. */
 int dlp_read_eligible(dlp_engine* e, uint8_t* eligible, int64_t n);

@@ -65,6 +65,7 @@ SIGNATURES = {
     "dlp_num_slots": (_int, [_p, _p, _p]),
     "dlp_read_labels": (_int, [_p, _p, _p, _i64]),
     "dlp_write_labels": (_int, [_p, _p, _i64]),
+    "dlp_harmonic_solve": (_int, [_p, _int, _i64, _p, _i64, _p]),
     "dlp_read_alive": (_int, [_p, _p, _i64]),
     "dlp_read_eligible": (_int, [_p, _p, _i64]),
     "dlp_graph_stats": (_int, [_p, _p, _p]),

@@ -43,7 +43,9 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str = Non
     lib = out or LIB
     if not force and not defines and lib == LIB and not _stale():
         return LIB
-    objdir = os.path.join(HERE, "_build" + ("_" + os.path.basename(lib).replace('.so', '') if lib != LIB else ""))
+    # variant builds keep their objects out of the package tree
+    objdir = os.path.join(HERE, "_build") if lib == LIB else \
+        os.path.join("/tmp", "dynlp_build_" + os.path.basename(lib).replace(".so", ""))
     os.makedirs(objdir, exist_ok=True)
 
     def compile_one(src):
@@ -61,7 +63,7 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str = Non
         for _, log in results:
             sys.stderr.write(log)
     tmp = lib + ".tmp"
-    cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs]
+    cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs, "-lcusolver"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

@@ -17,6 +17,8 @@
 #include <string>
 #include <vector>
 
+#include <cusolverDn.h>
+
 #include "engine.cuh"
 
 using namespace dlp;
@@ -616,7 +618,10 @@ int run_batch(dlp_engine* h, const dlp_config* cfg, const dlp_batch* batch, bool
             finish_time();
             return DLP_OK;
         }
-        bool full_cc = nd > 0 || !E.cc_valid;
+        // connectivity: incremental on insert-only batches, decremental
+        // (only the components that lost a vertex are rebuilt) after deletes,
+        // full rebuild when the union-find is stale (structure-only batches)
+        const int cc_mode = !E.cc_valid ? 2 : (nd > 0 ? 1 : 0);
         long long max_iter = cfg->max_iterations > 0 ? cfg->max_iterations
                                                       : std::max<long long>(1, 10 * E.num_alive);
         if (kind == KIND_DYNLP) {
@@ -626,7 +631,7 @@ int run_batch(dlp_engine* h, const dlp_config* cfg, const dlp_batch* batch, bool
                 intra_components_dev(E, bd, base);
                 init_components_dev(E, bd, base);
             }
-            reach_and_pin_dev(E, full_cc, n);
+            reach_and_pin_dev(E, cc_mode, n, bd.dels, nd);
             if (reduce) {  // component-sharded propagation
                 std::vector<ColCtl> col(E.ncol);
                 double ms = 0.0;
@@ -850,8 +855,9 @@ int dlp_destroy(dlp_engine* h) {
     cudaSetDevice(E.device);
     cudaStreamSynchronize(E.st);
     if (E.l2_persist) cudaCtxResetPersistingL2Cache();  // hand the carve-out's lines back
+    if (E.cusolver) cusolverDnDestroy((cusolverDnHandle_t)E.cusolver);
     DevArray<unsigned char>* u8s[] = {&E.alive, &E.mark, &E.root_gt, &E.owner_rank, &E.migr_from, &E.d_stage,
-                                      &E.cub_tmp};
+                                      &E.cub_tmp, &E.cc_hit_root, &E.cc_hit};
     E.migr_flag.release();
     E.migr_pos.release();
     E.migr_list.release();
@@ -929,6 +935,23 @@ int dlp_read_labels(dlp_engine* h, double* f, int8_t* gt, int64_t n) {
         }
         if (gt && n) DLP_CUDA_TRY(cudaMemcpyAsync(gt, E.gt.p, n, cudaMemcpyDeviceToHost, E.st));
         DLP_CUDA_TRY(cudaStreamSynchronize(E.st));
+    } catch (const CudaFailure& e) {
+        return cuda_fail(h, e);
+    }
+    return DLP_OK;
+}
+
+int dlp_harmonic_solve(dlp_engine* h, int stlp, int64_t dense_cap, double* f, int64_t n, int64_t* unreachable) {
+    Engine& E = h->E;
+    if (n != E.n_slots) return fail(E, DLP_EVALIDATION, "harmonic_solve: n=%lld but num_slots=%lld", (long long)n,
+                                    E.n_slots);
+    try {
+        DLP_CUDA_TRY(cudaSetDevice(E.device));
+        std::string msg;
+        long long fb = 0;
+        int rc = harmonic_solve_dev(E, stlp, dense_cap, f, &fb, &msg);
+        if (rc) return fail(E, rc, "%s", msg.c_str());
+        if (unreachable) *unreachable = fb;
     } catch (const CudaFailure& e) {
         return cuda_fail(h, e);
     }

@@ -178,6 +178,46 @@ struct RowAcc {
 };
 
 // ---------------------------------------------------------------------------
+// union-find (parents always point to smaller ids; root = minimum member)
+// ---------------------------------------------------------------------------
+__device__ inline int uf_find(int* par, int x) {
+    int cur = par[x];
+    if (cur != x) {
+        int prev = x, next;
+        while (cur > (next = ((volatile int*)par)[cur])) {
+            par[prev] = next;
+            prev = cur;
+            cur = next;
+        }
+    }
+    return cur;
+}
+
+// Root without path compression.  Flatten passes must not compress: a
+// concurrent compression store could overwrite a slot that another thread
+// has just set to its final root with a non-root ancestor.
+__device__ inline int uf_root(const int* par, int x) {
+    int cur = x, next;
+    while ((next = par[cur]) != cur) cur = next;
+    return cur;
+}
+
+__device__ inline void uf_unite(int* par, int a, int b) {
+    int ra = uf_find(par, a), rb = uf_find(par, b);
+    while (ra != rb) {
+        if (ra < rb) {
+            int t = ra;
+            ra = rb;
+            rb = t;
+        }
+        int old = atomicCAS(&par[ra], ra, rb);
+        if (old == ra) break;
+        ra = uf_find(par, old);
+        rb = uf_find(par, rb);
+    }
+}
+
+// ---------------------------------------------------------------------------
 // misc
 // ---------------------------------------------------------------------------
 __device__ inline unsigned long long dbits(double x) { return (unsigned long long)__double_as_longlong(x); }

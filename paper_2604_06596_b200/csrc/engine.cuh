@@ -188,6 +188,7 @@ struct Engine {
 
     // per-vertex ----------------------------------------------------------
     DevArray<unsigned char> alive, mark, root_gt, owner_rank, migr_from;
+    DevArray<unsigned char> cc_hit_root, cc_hit;  // decremental connectivity: hit roots / members
     DevArray<int> migr_flag, migr_pos, migr_list;
     DevArray<double> migr_buf;
     DevArray<int> purge_flag;
@@ -234,6 +235,8 @@ struct Engine {
     LPCtl* ctl = nullptr;
     PinnedArray<LPCtl> h_ctl;
     int lp_grid = 0;
+    void* cusolver = nullptr;  // cusolverDnHandle_t of the harmonic oracle (created on first use)
+    int lp_cert_hold = 1 << 30;  // certify alignment: max rounds a certify waits (DLP_CERT_HOLD)
     int l2_mode = 1;            // label L2 residency: 0 none, 1 persisting carve-out, 2 + access window
     size_t l2_persist = 0;      // persisting L2 carve-out (bytes)
     size_t l2_window_max = 0;
@@ -258,7 +261,10 @@ void apply_inserts_dev(Engine& E, const BatchDev& b, long long base);
 void resolve_tau_dev(Engine& E, double cfg_tau);
 void intra_components_dev(Engine& E, const BatchDev& b, long long base);
 void init_components_dev(Engine& E, const BatchDev& b, long long base);
-void reach_and_pin_dev(Engine& E, bool full_rebuild, long long n);
+// cc: 0 = incremental (union the batch's merged edges), 1 = decremental
+// (re-build only the components that lost a vertex, then add the batch's
+// edges; dels = the batch's deletes on the device), 2 = full rebuild
+void reach_and_pin_dev(Engine& E, int cc, long long n, const long long* dels = nullptr, long long nd = 0);
 void compact_pool(Engine& E, long long min_free);
 long long migr_collect(Engine& E, long long n);
 void migr_pack(Engine& E, long long m, double* dev_buf);
@@ -270,6 +276,9 @@ void lp_run_actions(Engine& E, double delta, bool first, bool cleanup);
 void lp_rows_apply(Engine& E, long long m, long long r_par);
 void lp_setup(Engine& E);
 void lp_dump_trace(Engine& E, long long rounds);
+// closed-form harmonic labels (harmonic.cu); out_host = C x n_slots
+int harmonic_solve_dev(Engine& E, int stlp, long long dense_cap, double* out_host, long long* fallback,
+                       std::string* msg);
 void itlp_active_dev(Engine& E, long long n);
 // readers (graph.cu) ----------------------------------------------------------
 void read_csr_dev(Engine& E, long long* indptr, long long* indices, double* weights, double* degrees);

@@ -95,46 +95,6 @@ void ensure_log(Engine& E, long long want) {
 }
 
 // ---------------------------------------------------------------------------
-// union-find (parents always point to smaller ids; root = minimum member)
-// ---------------------------------------------------------------------------
-__device__ inline int uf_find(int* par, int x) {
-    int cur = par[x];
-    if (cur != x) {
-        int prev = x, next;
-        while (cur > (next = ((volatile int*)par)[cur])) {
-            par[prev] = next;
-            prev = cur;
-            cur = next;
-        }
-    }
-    return cur;
-}
-
-// Root without path compression.  Flatten passes must not compress: a
-// concurrent compression store could overwrite a slot that another thread
-// has just set to its final root with a non-root ancestor.
-__device__ inline int uf_root(const int* par, int x) {
-    int cur = x, next;
-    while ((next = par[cur]) != cur) cur = next;
-    return cur;
-}
-
-__device__ inline void uf_unite(int* par, int a, int b) {
-    int ra = uf_find(par, a), rb = uf_find(par, b);
-    while (ra != rb) {
-        if (ra < rb) {
-            int t = ra;
-            ra = rb;
-            rb = t;
-        }
-        int old = atomicCAS(&par[ra], ra, rb);
-        if (old == ra) break;
-        ra = uf_find(par, old);
-        rb = uf_find(par, rb);
-    }
-}
-
-// ---------------------------------------------------------------------------
 // deletes (graph.py:311-326)
 // ---------------------------------------------------------------------------
 __global__ void k_kill(const long long* dels, long long nd, unsigned char* alive) {
@@ -960,6 +920,33 @@ __global__ void k_uf_union_merged(const int* lo, const int* hi, const DevState* 
         uf_unite(par, lo[i], hi[i]);
 }
 
+__global__ void k_cc_hit_roots(const long long* dels, long long nd, const int* par, unsigned char* hit_root) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nd; i += (long long)gridDim.x * blockDim.x)
+        hit_root[par[dels[i]]] = 1;
+}
+
+// members of a hit component become singletons (each thread owns parent[v];
+// the root's own entry is already v)
+__global__ void k_cc_reset_hit(long long n, int* par, const unsigned char* hit_root, unsigned char* hit) {
+    for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < n; v += (long long)gridDim.x * blockDim.x) {
+        const unsigned char h = hit_root[par[v]];
+        hit[v] = h;
+        if (h) par[v] = (int)v;
+    }
+}
+
+// surviving log edges of the hit components (both endpoints lie in the same
+// old component, so testing lo suffices; edges to this batch's new vertices
+// are also in the merged list)
+__global__ void k_uf_union_log_hit(const int* lo, const int* hi, const DevState* ds, const unsigned char* hit,
+                                   int* par) {
+    long long n = ds->log_n;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const int a = lo[i];
+        if (hit[a]) uf_unite(par, a, hi[i]);
+    }
+}
+
 __global__ void k_uf_flatten_root_gt(int* par, long long n, const unsigned char* alive, const signed char* gt,
                                      unsigned char* root_gt) {
     for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < n; v += (long long)gridDim.x * blockDim.x) {
@@ -1029,14 +1016,29 @@ __global__ void k_eligible(long long n, int ncol, long long cap, const unsigned 
     }
 }
 
-void reach_and_pin_dev(Engine& E, bool full_rebuild, long long n) {
+void reach_and_pin_dev(Engine& E, int cc, long long n, const long long* dels, long long nd) {
     cudaStream_t st = E.st;
     if (n == 0) return;
-    if (full_rebuild) {
+    if (cc == 2) {
         k_iota<<<grid_for(n), kBlock, 0, st>>>(E.parent.p, n);
         E.launches++;
         k_uf_union_log<<<grid_for(E.live_edges + 1), kBlock, 0, st>>>(E.log_lo.p, E.log_hi.p, E.ds, E.parent.p);
         E.launches++;
+    } else if (cc == 1 && nd > 0) {
+        // decremental: a component that lost no vertex lost no edge (an edge
+        // dies with an endpoint), so only components holding a deleted vertex
+        // can split.  Their members are reset to singletons and re-united over
+        // their surviving log edges; then the batch's new edges are added as
+        // in the incremental case.  (parent is flat: parent[v] = root.)
+        E.cc_hit_root.reserve(E.cap_n + 1, 0, st);
+        E.cc_hit.reserve(E.cap_n + 1, 0, st);
+        DLP_CUDA_TRY(cudaMemsetAsync(E.cc_hit_root.p, 0, n, st));
+        k_cc_hit_roots<<<grid_for(nd), kBlock, 0, st>>>(dels, nd, E.parent.p, E.cc_hit_root.p);
+        k_cc_reset_hit<<<grid_for(n), kBlock, 0, st>>>(n, E.parent.p, E.cc_hit_root.p, E.cc_hit.p);
+        k_uf_union_log_hit<<<grid_for(E.live_edges + 1), kBlock, 0, st>>>(E.log_lo.p, E.log_hi.p, E.ds, E.cc_hit.p,
+                                                                          E.parent.p);
+        k_uf_union_merged<<<E.sm_count * 8, kBlock, 0, st>>>(E.m_lo.p, E.m_hi.p, E.ds, E.parent.p);
+        E.launches += 4;
     } else {
         k_uf_union_merged<<<E.sm_count * 8, kBlock, 0, st>>>(E.m_lo.p, E.m_hi.p, E.ds, E.parent.p);
         E.launches++;

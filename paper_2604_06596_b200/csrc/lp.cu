@@ -56,6 +56,9 @@ constexpr int kLpThreads = 256;
 #ifndef DLP_WIN
 #define DLP_WIN 32
 #endif
+#ifndef DLP_WIN_MAX
+#define DLP_WIN_MAX 64  // window slots per warp tile (span-1 rounds; C-wide rounds fit kWin)
+#endif
 #ifndef DLP_HUB_WIN
 #define DLP_HUB_WIN 128
 #endif
@@ -117,6 +120,7 @@ struct LPParams {
     int itlp;
     int action_mode;  // execute ctl->act[] once per column, then exit (sharded batches)
     int cleanup;      // action mode: clear the leftover frontier masks and exit
+    int cert_hold;    // max rounds a column's certify sweep waits for the other columns
     // row-partitioned mode (one round per launch): work-item log of the round
     // (vertex, evaluated mask, changed mask), exchanged by the host
     int* log_u;
@@ -137,6 +141,7 @@ struct ColState {
     double max_change[kMaxCols];
     int converged[kMaxCols];
     unsigned int fr_mask, cert_mask;  // actions of the current round
+    int hold;  // rounds the waiting certify sweeps have been held (certify alignment)
     int done;
 };
 
@@ -294,6 +299,19 @@ __device__ void decide_actions(ColState& S, const LPParams& P, const unsigned lo
         ce |= bit;
         done = 0;
     }
+    // Certify alignment.  Columns are independent reference runs; the global
+    // round is only a schedule.  A column whose jacobi_run returned waits
+    // (does nothing: its frontier is empty and nothing it reads changes) while
+    // other columns still run frontier rounds, so the certify sweeps of
+    // several columns land in the same global round and share one gather of
+    // every eligible row instead of one full gather per column.  Per-column
+    // action sequences -- and so every result -- are unchanged.
+    if (!P.itlp && ce && fr && S.hold < P.cert_hold) {
+        S.hold++;
+        ce = 0;
+    } else {
+        S.hold = 0;
+    }
     S.fr_mask = fr;
     S.cert_mask = ce;
     S.done = done;
@@ -353,7 +371,7 @@ struct BlockCounters {
 struct WarpTile {
     long long st[32];
     int u[32], len[32], off[33];
-    unsigned int em[32];
+    unsigned int em[32], chg[32];
 };
 
 __device__ inline int tile_row_of(const int* off, int nrows, int g) {
@@ -368,6 +386,40 @@ __device__ inline int tile_row_of(const int* off, int nrows, int g) {
     return lo;
 }
 
+// Round geometry, set with the round's actions (every CTA's controller):
+// the active columns (frontier | certify) and the step-major tile shape.
+// A warp tile holds rpt = 32 / na rows and lane (r, a) runs row r's ordered
+// sums for active column acol[a]; a window stages S consecutive entries of
+// EVERY row of the tile, so all lanes advance together (a certify round of
+// one column packs 32 rows per warp instead of idling 31 lanes).  Label
+// words are copied as one 8-byte word per entry when a single column is
+// active (span 1), else as the whole C-wide row.
+struct TileGeo {
+    int na, rpt, S, cmin, span;
+    int acol[kMaxCols];
+};
+constexpr int kMaxQ = DLP_WIN_MAX / 32;  // window slots per gathering lane
+// warp-private staging (doubles): DLP_WIN_MAX weights + kWin C-wide label rows
+__host__ __device__ inline int warp_smem_doubles(int C) { return DLP_WIN_MAX + (kWin * C > DLP_WIN_MAX ? kWin * C : DLP_WIN_MAX); }
+
+#ifndef DLP_LONG_RPT
+#define DLP_LONG_RPT 1  // rows per long-row tile (length imbalance wastes windows when > 1)
+#endif
+__device__ inline void set_geo(TileGeo& G, unsigned int act, int C, int xcap, int max_rows) {
+    int na = 0;
+    for (int c = 0; c < C; c++)
+        if ((act >> c) & 1u) G.acol[na++] = c;
+    if (na == 0) G.acol[na++] = 0;  // idle round (the loop is about to end)
+    G.na = na;
+    G.rpt = min(32 / na, max_rows);
+    G.cmin = na == 1 ? G.acol[0] : 0;
+    G.span = na == 1 ? 1 : C;
+    int we = xcap / G.span;  // label words fit in xcap doubles, weights in DLP_WIN_MAX
+    if (we > DLP_WIN_MAX) we = DLP_WIN_MAX;
+    int S = we / G.rpt;
+    G.S = S < 1 ? 1 : S;
+}
+
 // Round context shared by the tile routine.
 struct RoundCtx {
     const int* W;           // work list of this row class
@@ -378,10 +430,6 @@ struct RoundCtx {
     unsigned long long* tmax;  // trace: longest evaluated row of the round (or null)
 };
 
-// Evaluate `nrows` consecutive work items W[k0 ..] as one warp tile:
-// entry-parallel gathers staged in warp-private shared memory (product terms
-// precomputed), then lane (row, column) runs the ordered sums; finally the
-// changed rows claim themselves and their neighbours.
 // Row metadata of one tile row (lane r holds row r): loads issued one tile
 // ahead so their latency hides behind the current tile's gathers.
 struct TileMeta {
@@ -399,13 +447,43 @@ __device__ inline TileMeta load_meta(const LPParams& P, const RoundCtx& R, int u
     return m;
 }
 
-// Evaluate the tile (rows W[k0 ..], metadata m); `un` is the next tile's row
-// of this lane (-1 if none), whose metadata is loaded into *mn mid-tile.
-__device__ void warp_tile(const LPParams& P, const RoundCtx& R, ClaimCtx& K, BlockCounters& B, WarpTile& T,
-                          double* sw, double* sx, double* sfu, long long k0, int nrows, unsigned long long pol,
-                          const TileMeta& m, int un, TileMeta* mn) {
+// Per-lane constants of a round's geometry: the window slots this lane
+// gathers (slot j = lane + 32q -> tile row j / S, step j % S) and the
+// accumulate role (row ar, column ac).
+struct LaneGeo {
+    int qr[kMaxQ], qs[kMaxQ];
+    int ar, ac, acs;  // row, column, column offset inside the copied span
+    bool alane;       // lane has an accumulate role
+};
+__device__ inline LaneGeo lane_geo(const TileGeo& G, int lane) {
+    LaneGeo L;
+#pragma unroll
+    for (int q = 0; q < kMaxQ; q++) {
+        const int j = lane + 32 * q;
+        L.qr[q] = j < G.rpt * G.S ? j / G.S : 32;
+        L.qs[q] = j - (j / G.S) * G.S;
+    }
+    L.alane = lane < G.rpt * G.na;
+    L.ar = lane / G.na;
+    L.ac = G.acol[lane - L.ar * G.na];
+    L.acs = L.ac - G.cmin;
+    return L;
+}
+
+// Evaluate `nrows` consecutive work items W[k0 ..] as one step-major warp
+// tile (metadata m: lane r holds row r); `un` is the next tile's row of this
+// lane (-1 if none), whose metadata is loaded into *mn mid-tile.  Gathers are
+// entry-parallel into warp-private shared memory (ids and weights one window
+// ahead, label words by cp.async), then lane (row, column) runs the row's
+// sums in stored order (kernels/_csr.pyx:38-52); finally the changed rows
+// claim themselves and their neighbours (_csr.pyx:175-191).
+__device__ void warp_tile(const LPParams& P, const RoundCtx& R, const TileGeo& G, ClaimCtx& K,
+                          BlockCounters& B, WarpTile& T, double* sw, double* sx, long long k0, int nrows,
+                          unsigned long long pol, const TileMeta& m, int un, TileMeta* mn) {
     const int C = P.C;
+    const LaneGeo L = lane_geo(G, threadIdx.x & 31);
     const int lane = threadIdx.x & 31;
+    const int S = G.S, span = G.span;
     // ---- tile rows
     int len = 0;
     unsigned int em = 0;
@@ -417,17 +495,15 @@ __device__ void warp_tile(const LPParams& P, const RoundCtx& R, ClaimCtx& K, Blo
         T.em[lane] = em;
         T.st[lane] = em ? m.st : 0;
         T.len[lane] = len;
+        T.chg[lane] = 0u;
     }
-    __syncwarp();  // T.* written by lane r is read by other lanes below
-    int incl = len;
+    int maxlen = len, total = len;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        int y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
+    for (int o = 16; o > 0; o >>= 1) {
+        maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, o));
+        total += __shfl_xor_sync(0xffffffffu, total, o);
     }
-    if (lane < nrows) T.off[lane] = incl - len;
     if (R.tmax && len) atomicMax(R.tmax, (unsigned long long)len);
-    const int total = __shfl_sync(0xffffffffu, incl, 31);
     {
         unsigned int nz = __ballot_sync(0xffffffffu, em != 0);
         if (lane == 0 && nz) {
@@ -435,133 +511,138 @@ __device__ void warp_tile(const LPParams& P, const RoundCtx& R, ClaimCtx& K, Blo
             atomicAdd(&B.uent, (unsigned long long)total);
         }
     }
-    // own label rows ride with the first window's asynchronous copies
-    if (lane < nrows && T.em[lane]) copy_label_row(sfu + lane * C, P.X + (long long)T.u[lane] * C, C, pol);
+    __syncwarp();  // T.* written by lane r is read by other lanes below
+    // accumulate role: lane (ar, ac); its own label fu is a plain load whose
+    // latency overlaps the first window's gathers
+    const bool aact = L.alane && L.ar < nrows && ((T.em[L.ar] >> L.ac) & 1u);
+    const int u_a = aact ? T.u[L.ar] : 0;
+    const int len_a = aact ? T.len[L.ar] : 0;
+    const double fu = aact ? ld_keep(P.X + (long long)u_a * C + L.ac, pol) : 0.0;
+    // gather role: slot q of this lane -> (row qr, step qs)
+    long long qst[kMaxQ];
+    int qlen[kMaxQ];
+#pragma unroll
+    for (int q = 0; q < kMaxQ; q++) {
+        const bool ok = L.qr[q] < nrows;
+        qst[q] = ok ? T.st[L.qr[q]] + L.qs[q] : 0;
+        qlen[q] = ok ? T.len[L.qr[q]] - L.qs[q] : 0;  // window wb is valid while wb < qlen
+    }
     *mn = load_meta(P, R, un);  // next tile's metadata, consumed next iteration
-    __syncwarp();
-    // ---- accumulate lanes
-    const int ar = lane / C, ac = lane - ar * C;
-    const bool aact = ar < nrows && ((T.em[ar] >> ac) & 1u);
     RowAcc acc;
     acc.init();
-    const int a_lo = aact ? T.off[ar] : 0, a_hi = aact ? T.off[ar] + T.len[ar] : 0;
-    // ids / weights of a window are loaded one window ahead (software pipeline):
-    // a window costs one dependent round trip (the label gathers)
-    int vv[kWin / 32], rr[kWin / 32];
-    double ww[kWin / 32];
+    int vv[kMaxQ];
+    double ww[kMaxQ];
     auto load_ids = [&](int wb) {
-        const int wn = min(kWin, total - wb);
 #pragma unroll
-        for (int j = 0; j < kWin / 32; j++) {
-            int i = lane + 32 * j;
-            rr[j] = -1;
-            if (i < wn) {
-                int g = wb + i;
-                int r = tile_row_of(T.off, nrows, g);
-                long long p = T.st[r] + (g - T.off[r]);
-                rr[j] = r;
-                vv[j] = __ldcs(P.nbr + p);
-                ww[j] = __ldcs(P.w + p);
+        for (int q = 0; q < kMaxQ; q++) {
+            if (wb < qlen[q]) {
+                vv[q] = __ldcs(P.nbr + qst[q] + wb);
+                ww[q] = __ldcs(P.w + qst[q] + wb);
             }
         }
     };
-    if (total > 0) load_ids(0);
-    for (int wb = 0; wb < total; wb += kWin) {
-        const int wn = min(kWin, total - wb);
-        // label rows: asynchronous copies straight into shared memory, so every
-        // gather of the window is in flight at once (no register dependency)
+    if (maxlen > 0) load_ids(0);
+    const double* xcol = P.X + G.cmin;
+    for (int wb = 0; wb < maxlen; wb += S) {
 #pragma unroll
-        for (int j = 0; j < kWin / 32; j++) {
-            if (rr[j] < 0) continue;
-            int i = lane + 32 * j;
-            sw[i] = ww[j];
-            copy_label_row(sx + i * C, P.X + (long long)vv[j] * C, C, pol);
+        for (int q = 0; q < kMaxQ; q++) {
+            if (wb >= qlen[q]) continue;
+            const int j = lane + 32 * q;
+            sw[j] = ww[q];
+            if (span == 1)
+                cp_async8(sx + j, xcol + (long long)vv[q] * C, pol);
+            else
+                copy_label_row(sx + j * span, P.X + (long long)vv[q] * C, C, pol);
         }
-        if (wb + kWin < total) load_ids(wb + kWin);
+        if (wb + S < maxlen) load_ids(wb + S);
         cp_async_wait_all();
         __syncwarp();
         if (aact) {
-            const double fu = sfu[ar * C + ac];
-            const int lo = max(a_lo, wb) - wb, hi = min(a_hi, wb + wn) - wb;
-            int t = lo;
-            for (; t + kAccUnroll <= hi; t += kAccUnroll) acc.add_boxed_block<kAccUnroll>(sw + t, sx + t * C + ac, C, fu);
-            for (; t < hi; t++) acc.add_boxed(sw[t], sx[t * C + ac], fu);
+            const int hi = min(S, len_a - wb);
+            const double* w0p = sw + L.ar * S;
+            const double* x0p = sx + (L.ar * S) * span + L.acs;
+            int t = 0;
+            for (; t + kAccUnroll <= hi; t += kAccUnroll) acc.add_boxed_block<kAccUnroll>(w0p + t, x0p + t * span, span, fu);
+            for (; t < hi; t++) acc.add_boxed(w0p[t], x0p[t * span], fu);
         }
-        __syncwarp();
-    }
-    if (total == 0) {  // no window ran: the own-label copies must still land
-        cp_async_wait_all();
         __syncwarp();
     }
     // ---- finish: stage, count, flag
     unsigned int ch = 0;
     if (aact) {
-        const int u = T.u[ar];
-        const double fu = sfu[ar * C + ac];
+        const int c = L.ac;
         double val;
         double d = acc.finish(fu, &val);
-        __stcs(P.Y + (R.ybase + k0 + ar) * C + ac, val);
+        __stcs(P.Y + (R.ybase + k0 + L.ar) * C + c, val);
         K.c_nev++;
-        K.c_edg += (unsigned long long)T.len[ar];
+        K.c_edg += (unsigned long long)len_a;
         if (d < 0.0) {  // isolated sentinel (_csr.pyx:49-51, 170-173)
             K.c_warn++;
-            atomicAnd(&P.eligm[u], ~(1u << ac));
-            atomicAdd((unsigned long long*)&P.ctl->elig_count[ac], ~0ULL);
+            atomicAnd(&P.eligm[u_a], ~(1u << c));
+            atomicAdd((unsigned long long*)&P.ctl->elig_count[c], ~0ULL);
         } else {
             K.c_rmax = fmax(K.c_rmax, d);
-            if (!P.itlp && d > P.delta) ch = 1u << ac;
+            if (!P.itlp && d > P.delta) ch = 1u << c;
         }
     }
     if (P.itlp) return;
     // ---- expand (jacobi_run commit loop, _csr.pyx:175-191)
-    const unsigned int bal = __ballot_sync(0xffffffffu, ch != 0);
-    if (!bal) return;
-    const unsigned int cmask = C >= 32 ? 0xffffffffu : ((1u << C) - 1u);
-    // lane (row, c) can only flag column c: a row's mask is its slice of the ballot
-    if (lane < nrows) {
-        unsigned int m = (bal >> (lane * C)) & cmask;
-        if (m) {
-            K.claimed |= m;  // u changed, so u itself is eligible for those columns
-            if (P.log_chg) P.log_chg[R.ybase + k0 + lane] = m;
-            if (R.scan_mode)
-                atomicOr(&K.fm_next[T.u[lane]], m);
-            else
-                claim(K, T.u[lane], m);
-        }
+    if (!__any_sync(0xffffffffu, ch != 0)) return;
+    if (ch) atomicOr(&T.chg[L.ar], ch);
+    __syncwarp();
+    unsigned int mrow = lane < nrows ? T.chg[lane] : 0u;
+    if (mrow) {
+        K.claimed |= mrow;  // u changed, so u itself is eligible for those columns
+        if (P.log_chg) P.log_chg[R.ybase + k0 + lane] = mrow;
+        if (R.scan_mode)
+            atomicOr(&K.fm_next[T.u[lane]], mrow);
+        else
+            claim(K, T.u[lane], mrow);
     }
-    if (kExpandRegs && total <= kWin) {
+    if (maxlen <= S) {
         // single-window tile: the gathering lanes still hold the entries' ids
 #pragma unroll
-        for (int j = 0; j < kWin / 32; j++) {
-            if (rr[j] < 0) continue;
-            const unsigned int m = (bal >> (rr[j] * C)) & cmask;
-            if (!m) continue;
+        for (int q = 0; q < kMaxQ; q++) {
+            if (qlen[q] <= 0) continue;
+            const unsigned int mq = T.chg[L.qr[q]];
+            if (!mq) continue;
             if (R.scan_mode)
-                atomicOr(&K.fm_next[vv[j]], m);  // no return value: a fire-and-forget RED
+                atomicOr(&K.fm_next[vv[q]], mq);  // no return value: a fire-and-forget RED
             else
-                claim(K, vv[j], m);
+                claim(K, vv[q], mq);
         }
         return;
     }
-    for (int g = lane; g < total; g += 32) {
+    // multi-window tile: walk the changed rows' entries, flattened
+    const int clen = mrow ? len : 0;
+    int incl = clen;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane < nrows) T.off[lane] = incl - clen;
+    const int ctot = __shfl_sync(0xffffffffu, incl, 31);
+    __syncwarp();
+    for (int g = lane; g < ctot; g += 32) {
         int r = tile_row_of(T.off, nrows, g);
-        unsigned int m = (bal >> (r * C)) & cmask;
-        if (!m) continue;
+        const unsigned int mq = T.chg[r];
         int v = __ldcs(P.nbr + T.st[r] + (g - T.off[r]));
         if (R.scan_mode)
-            atomicOr(&K.fm_next[v], m);  // no return value: a fire-and-forget RED
+            atomicOr(&K.fm_next[v], mq);
         else
-            claim(K, v, m);
+            claim(K, v, mq);
     }
 }
 
 // Warp loop over the tiles of one row class: tile indices are grabbed two
 // ahead and row metadata one ahead (software pipeline), so a tile's
 // dependent chain of loads overlaps the previous tile's gathers.
-__device__ void warp_tiles(const LPParams& P, const RoundCtx& R, ClaimCtx& K, BlockCounters& B, WarpTile& T,
-                           double* sw, double* sx, double* sfu, unsigned int* grab, long long nitems, int per,
-                           unsigned long long pol) {
+__device__ void warp_tiles(const LPParams& P, const RoundCtx& R, const TileGeo& G, ClaimCtx& K,
+                           BlockCounters& B, WarpTile& T, double* sw, double* sx, unsigned int* grab,
+                           long long nitems, unsigned long long pol) {
     const int lane = threadIdx.x & 31;
+    const int per = G.rpt;
     if (nitems <= 0) return;
     unsigned int kr = 0;
     if (lane == 0) kr = atomicAdd(grab, (unsigned int)per);
@@ -576,284 +657,12 @@ __device__ void warp_tiles(const LPParams& P, const RoundCtx& R, ClaimCtx& K, Bl
         const int un = lane < nrn ? R.W[kn + lane] : -1;
         if (lane == 0 && kn < nitems) kr = atomicAdd(grab, (unsigned int)per);
         TileMeta mn;
-        warp_tile(P, R, K, B, T, sw, sx, sfu, k, nr, pol, m, un, &mn);
+        warp_tile(P, R, G, K, B, T, sw, sx, k, nr, pol, m, un, &mn);
         __syncwarp();
         if (kn >= nitems) break;
         k = kn;
         nr = nrn;
         m = mn;
-    }
-}
-
-// ---------------------------------------------------------------------------
-// Producer / consumer warp pairs (DLP_PC): warps 0-3 only gather, warps 4-7
-// only sum.  A producer takes tiles (same tiles as warp_tiles), stages each
-// 64-entry chunk -- row metadata, ids, weights and the label vectors by
-// cp.async -- into a 2-slot ring shared with its consumer and signals the
-// slot's mbarrier when the copies land (cp.async.mbarrier.arrive.noinc), so
-// it can move on to the next chunk's id loads at once; the consumer runs the
-// ordered sums, finishes the rows and expands.  Memory and the dependent
-// fp64 chains overlap instead of alternating inside one warp.
-// ---------------------------------------------------------------------------
-constexpr int PC_FIRST = 1, PC_LAST = 2, PC_DONE = 4;
-constexpr int kPCSlots = 2;
-
-__host__ __device__ inline size_t pc_slot_bytes(int C) {
-    size_t b = 64 + 4 * (32 + 32 + 40 + 32) + 8 * 32 + 8 * 32 + 4 * (size_t)kWin + 8 * (size_t)kWin +
-               8 * (size_t)kWin * C;
-    return (b + 127) & ~(size_t)127;
-}
-
-struct PCSlot {
-    int* hdr;  // nrows, e0, e1, flags, total
-    long long* ybase;
-    int *u, *off, *len;
-    unsigned int* em;
-    long long* st;
-    double* fu;
-    int* nbr;
-    double *w, *x;
-};
-
-__device__ inline PCSlot pc_slot(unsigned char* base) {
-    PCSlot s;
-    s.hdr = (int*)base;
-    s.ybase = (long long*)(base + 32);
-    s.u = (int*)(base + 64);
-    s.em = (unsigned int*)(s.u + 32);
-    s.off = (int*)(s.em + 32);
-    s.len = s.off + 40;
-    s.st = (long long*)(s.len + 32);
-    s.fu = (double*)(s.st + 32);
-    s.nbr = (int*)(s.fu + 32);
-    s.w = (double*)(s.nbr + kWin);
-    s.x = s.w + kWin;
-    return s;
-}
-
-__device__ inline void mbar_init_s(unsigned long long* b, unsigned int count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned int)__cvta_generic_to_shared(b)),
-                 "r"(count)
-                 : "memory");
-}
-__device__ inline void mbar_arrive_s(unsigned long long* b) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"((unsigned int)__cvta_generic_to_shared(b))
-                 : "memory");
-}
-__device__ inline void mbar_arrive_cp(unsigned long long* b) {  // when this thread's cp.asyncs land
-    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(
-                     (unsigned int)__cvta_generic_to_shared(b))
-                 : "memory");
-}
-__device__ inline void mbar_wait_s(unsigned long long* b, unsigned int parity) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n"
-        "PCW_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra PCW_%=;\n}" ::"r"((unsigned int)__cvta_generic_to_shared(b)),
-        "r"(parity)
-        : "memory");
-}
-
-struct PCRing {
-    unsigned char* base;  // kPCSlots slots of pc_slot_bytes(C)
-    unsigned long long* full;
-    unsigned long long* empty;
-    size_t sb;
-    int s;
-    unsigned int ph;
-    __device__ inline unsigned char* cur() const { return base + (size_t)s * sb; }
-    __device__ inline void advance() {
-        if (++s == kPCSlots) {
-            s = 0;
-            ph ^= 1;
-        }
-    }
-};
-
-// producer: stage every chunk of the tiles of one row class
-__device__ void pc_produce_class(const LPParams& P, const RoundCtx& R, unsigned int* grab, long long nitems, int per,
-                                 PCRing& ring, unsigned long long pol) {
-    const int C = P.C;
-    const int lane = threadIdx.x & 31;
-    if (nitems <= 0) return;
-    unsigned int kr = 0;
-    if (lane == 0) kr = atomicAdd(grab, (unsigned int)per);
-    long long k = __shfl_sync(0xffffffffu, kr, 0);
-    if (k >= nitems) return;
-    int nr = (int)min((long long)per, nitems - k);
-    TileMeta m = load_meta(P, R, lane < nr ? R.W[k + lane] : -1);
-    if (lane == 0) kr = atomicAdd(grab, (unsigned int)per);
-    for (;;) {
-        const long long kn = __shfl_sync(0xffffffffu, kr, 0);
-        const int nrn = kn < nitems ? (int)min((long long)per, nitems - kn) : 0;
-        const int un = lane < nrn ? R.W[kn + lane] : -1;
-        if (lane == 0 && kn < nitems) kr = atomicAdd(grab, (unsigned int)per);
-        // ---- tile k: rows in registers, offsets by a warp scan
-        unsigned int em = 0;
-        int len = 0;
-        long long st = 0;
-        if (lane < nr) {
-            em = m.em;
-            P.emask_store[R.ybase + k + lane] = em;
-            len = em ? m.len : 0;
-            st = em ? m.st : 0;
-        }
-        int incl = len;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            int y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
-        }
-        const int off = incl - len;
-        const int total = __shfl_sync(0xffffffffu, incl, 31);
-        TileMeta mn = load_meta(P, R, un);  // next tile's metadata, consumed next iteration
-        const int nch = total > 0 ? (total + kWin - 1) / kWin : 1;
-        for (int ch = 0; ch < nch; ch++) {
-            const int e0 = ch * kWin, e1 = min(total, e0 + kWin);
-            mbar_wait_s(&ring.empty[ring.s], ring.ph ^ 1);
-            PCSlot S = pc_slot(ring.cur());
-            if (lane == 0) {
-                S.hdr[0] = nr;
-                S.hdr[1] = e0;
-                S.hdr[2] = e1;
-                S.hdr[3] = (ch == 0 ? PC_FIRST : 0) | (ch == nch - 1 ? PC_LAST : 0);
-                S.hdr[4] = total;
-                *S.ybase = R.ybase + k;
-            }
-            if (lane < nr) {
-                S.u[lane] = m.u;
-                S.em[lane] = em;
-                S.off[lane] = off;
-                S.len[lane] = len;
-                S.st[lane] = st;
-                if (ch == 0 && em) copy_label_row(S.fu + lane * C, P.X + (long long)m.u * C, C, pol);
-            }
-            __syncwarp();
-#pragma unroll
-            for (int j = 0; j < kWin / 32; j++) {
-                const int i = lane + 32 * j;
-                if (i < e1 - e0) {
-                    const int g = e0 + i;
-                    const int r = tile_row_of(S.off, nr, g);
-                    const long long p = S.st[r] + (g - S.off[r]);
-                    const int v = __ldcs(P.nbr + p);
-                    S.nbr[i] = v;
-                    S.w[i] = __ldcs(P.w + p);
-                    copy_label_row(S.x + i * C, P.X + (long long)v * C, C, pol);
-                }
-            }
-            __syncwarp();
-            mbar_arrive_cp(&ring.full[ring.s]);
-            if (lane == 0) mbar_arrive_s(&ring.full[ring.s]);
-            ring.advance();
-        }
-        if (kn >= nitems) break;
-        k = kn;
-        nr = nrn;
-        m = mn;
-    }
-}
-
-__device__ void pc_produce_done(PCRing& ring) {
-    const int lane = threadIdx.x & 31;
-    mbar_wait_s(&ring.empty[ring.s], ring.ph ^ 1);
-    PCSlot S = pc_slot(ring.cur());
-    if (lane == 0) S.hdr[3] = PC_DONE;
-    __syncwarp();
-    mbar_arrive_cp(&ring.full[ring.s]);
-    if (lane == 0) mbar_arrive_s(&ring.full[ring.s]);
-    ring.advance();
-}
-
-// consumer: ordered sums, finish and expand for every staged chunk
-__device__ void pc_consume(const LPParams& P, bool scan_mode, ClaimCtx& K, BlockCounters& B, PCRing& ring) {
-    const int C = P.C;
-    const int lane = threadIdx.x & 31;
-    const int ar = lane / C, ac = lane - ar * C;
-    RowAcc acc;
-    bool aact = false;
-    double fu = 0.0;
-    int a_lo = 0, a_hi = 0;
-    for (;;) {
-        mbar_wait_s(&ring.full[ring.s], ring.ph);
-        PCSlot S = pc_slot(ring.cur());
-        const int flags = S.hdr[3];
-        if (flags & PC_DONE) {
-            __syncwarp();
-            if (lane == 0) mbar_arrive_s(&ring.empty[ring.s]);
-            ring.advance();
-            break;
-        }
-        const int nr = S.hdr[0], e0 = S.hdr[1], e1 = S.hdr[2];
-        if (flags & PC_FIRST) {
-            aact = ar < nr && ((S.em[ar] >> ac) & 1u);
-            acc.init();
-            a_lo = aact ? S.off[ar] : 0;
-            a_hi = aact ? S.off[ar] + S.len[ar] : 0;
-            fu = aact ? S.fu[ar * C + ac] : 0.0;
-        }
-        if (aact) {
-            const int lo = max(a_lo, e0) - e0, hi = min(a_hi, e1) - e0;
-#pragma unroll kAccUnroll
-            for (int t = lo; t < hi; t++) acc.add_boxed(S.w[t], S.x[t * C + ac], fu);
-        }
-        if (flags & PC_LAST) {
-            unsigned int ch = 0;
-            if (aact) {
-                const int u = S.u[ar];
-                double val;
-                double d = acc.finish(fu, &val);
-                __stcs(P.Y + (*S.ybase + ar) * C + ac, val);
-                K.c_nev++;
-                K.c_edg += (unsigned long long)S.len[ar];
-                if (d < 0.0) {  // isolated sentinel (_csr.pyx:49-51, 170-173)
-                    K.c_warn++;
-                    atomicAnd(&P.eligm[u], ~(1u << ac));
-                    atomicAdd((unsigned long long*)&P.ctl->elig_count[ac], ~0ULL);
-                } else {
-                    K.c_rmax = fmax(K.c_rmax, d);
-                    if (!P.itlp && d > P.delta) ch = 1u << ac;
-                }
-            }
-            {
-                unsigned int nz = __ballot_sync(0xffffffffu, lane < nr && S.em[lane] != 0);
-                if (lane == 0 && nz) {
-                    atomicAdd(&B.urows, (unsigned long long)__popc(nz));
-                    atomicAdd(&B.uent, (unsigned long long)S.hdr[4]);
-                }
-            }
-            if (!P.itlp) {
-                const unsigned int bal = __ballot_sync(0xffffffffu, ch != 0);
-                if (bal) {
-                    const unsigned int cmask = C >= 32 ? 0xffffffffu : ((1u << C) - 1u);
-                    const int total = S.hdr[4];
-                    if (lane < nr) {
-                        unsigned int mm = (bal >> (lane * C)) & cmask;
-                        if (mm) {
-                            K.claimed |= mm;
-                            if (scan_mode)
-                                atomicOr(&K.fm_next[S.u[lane]], mm);
-                            else
-                                claim(K, S.u[lane], mm);
-                        }
-                    }
-                    for (int g = lane; g < total; g += 32) {
-                        int r = tile_row_of(S.off, nr, g);
-                        unsigned int mm = (bal >> (r * C)) & cmask;
-                        if (!mm) continue;
-                        int v = __ldcs(P.nbr + S.st[r] + (g - S.off[r]));
-                        if (scan_mode)
-                            atomicOr(&K.fm_next[v], mm);
-                        else
-                            claim(K, v, mm);
-                    }
-                }
-            }
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive_s(&ring.empty[ring.s]);
-        ring.advance();
     }
 }
 
@@ -1089,6 +898,7 @@ __device__ inline void gsync(LPCtl* ctl, unsigned int& target) { grid_sync(&ctl-
 __global__ void __launch_bounds__(kLpThreads, DLP_LP_MINB) k_lp_fused(LPParams P) {
     extern __shared__ double smem_dyn[];
     __shared__ ColState S;
+    __shared__ TileGeo s_geo, s_geo_l;  // short-row / long-row tile shapes
     __shared__ BlockCounters B;
     __shared__ WarpTile TT[kLpThreads / 32];
     __shared__ unsigned long long s_res[4 * kMaxCols];
@@ -1097,9 +907,6 @@ __global__ void __launch_bounds__(kLpThreads, DLP_LP_MINB) k_lp_fused(LPParams P
     __shared__ int s_i[4];
     __shared__ unsigned int s_u32[4], s_claimed, s_cnt[3], s_base[3];
     __shared__ unsigned int s_wc[3][kLpThreads / 32];
-#ifdef DLP_PC
-    __shared__ unsigned long long pc_full[4][kPCSlots], pc_empty[4][kPCSlots];
-#endif
 
     const int C = P.C;
     const int tid = threadIdx.x;
@@ -1108,29 +915,14 @@ __global__ void __launch_bounds__(kLpThreads, DLP_LP_MINB) k_lp_fused(LPParams P
     const long long gth = (long long)gridDim.x * blockDim.x;
     LPCtl* ctl = P.ctl;
     unsigned int target = 0;
-    const int wsm = kWin * (C + 1) + 32;  // doubles of warp-private staging
+    const int wsm = warp_smem_doubles(C);  // warp-private staging: weights, then label words
     double* sw = smem_dyn + warp * wsm;
-    double* sx = sw + kWin;
-    double* sfu = sx + kWin * C;
+    double* sx = sw + DLP_WIN_MAX;
     WarpTile& T = TT[warp];
     const unsigned int allc = C >= 32 ? 0xffffffffu : ((1u << C) - 1u);
     const unsigned long long pol = l2_evict_last_policy();
-    const int rpw = 32 / C;  // rows per short tile
     const long long n = P.n;
 
-#ifdef DLP_PC
-    if (tid == 0) {
-        for (int p = 0; p < 4; p++)
-            for (int q = 0; q < kPCSlots; q++) {
-                mbar_init_s(&pc_full[p][q], 33);
-                mbar_init_s(&pc_empty[p][q], 1);
-            }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    PCRing ring{(unsigned char*)smem_dyn + (size_t)(warp & 3) * kPCSlots * pc_slot_bytes(C), pc_full[warp & 3],
-                pc_empty[warp & 3], pc_slot_bytes(C), 0, 0u};
-#endif
     // ---- prologue: F0 (engine.py:364-367) is every column's first frontier;
     // the eligible list and F0 are split by row class.  In action mode only
     // the first launch of a batch runs it; later launches resume the lists.
@@ -1173,6 +965,7 @@ __global__ void __launch_bounds__(kLpThreads, DLP_LP_MINB) k_lp_fused(LPParams P
             if (P.action_mode && (P.cleanup || ctl->act[c] == ACT_NONE)) S.phase[c] = PH_DONE;
         }
         S.fr_mask = S.cert_mask = 0;
+        S.hold = 0;
         if (blockIdx.x == 0 && !resume)
             for (int c = 0; c < C; c++) ctl->elig_count[c] = n_el;
     }
@@ -1182,6 +975,8 @@ __global__ void __launch_bounds__(kLpThreads, DLP_LP_MINB) k_lp_fused(LPParams P
             decide_actions_act(S, P, nullptr, nullptr, 1);
         else
             decide_actions(S, P, nullptr, nullptr, 1);
+        set_geo(s_geo, S.fr_mask | S.cert_mask, C, wsm - DLP_WIN_MAX, 32);
+        set_geo(s_geo_l, S.fr_mask | S.cert_mask, C, wsm - DLP_WIN_MAX, DLP_LONG_RPT);
     }
     long long nel[3], ncur[3];
     for (int j = 0; j < 3; j++) {
@@ -1248,25 +1043,11 @@ __global__ void __launch_bounds__(kLpThreads, DLP_LP_MINB) k_lp_fused(LPParams P
             }
             RoundCtx RL{W1, n0c, FR, CE, fm_cur, scan_mode, tmax};
             RoundCtx RS{W0, 0, FR, CE, fm_cur, scan_mode, tmax};
-#ifdef DLP_PC
-            if (warp < 4) {
-                pc_produce_class(P, RL, &slot->grab[1], n1c, 1, ring, pol);  // long rows: one per tile
-                pc_produce_class(P, RS, &slot->grab[0], n0c, rpw, ring, pol);  // short rows
-                pc_produce_done(ring);
-            } else {
-                pc_consume(P, scan_mode, K, B, ring);
-            }
-            (void)T;
-#else
             if (prof) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tw1));
-#ifndef DLP_LONG_PER
-#define DLP_LONG_PER 1
-#endif
-            warp_tiles(P, RL, K, B, T, sw, sx, sfu, &slot->grab[1], n1c, DLP_LONG_PER, pol);  // long rows
+            warp_tiles(P, RL, s_geo_l, K, B, T, sw, sx, &slot->grab[1], n1c, pol);  // long rows
             if (prof) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tw2));
-            warp_tiles(P, RS, K, B, T, sw, sx, sfu, &slot->grab[0], n0c, rpw, pol);  // short rows
+            warp_tiles(P, RS, s_geo, K, B, T, sw, sx, &slot->grab[0], n0c, pol);  // short rows
             if (prof) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tw3));
-#endif
             if (prof) {  // warp-time per part of phase 1 (diagnostics)
                 atomicAdd(&ctl->prof[0], tw1 - tw0);
                 atomicAdd(&ctl->prof[1], tw2 - tw1);
@@ -1274,8 +1055,8 @@ __global__ void __launch_bounds__(kLpThreads, DLP_LP_MINB) k_lp_fused(LPParams P
             }
         }
         if (K.claimed) atomicOr(&B.claimed, K.claimed);
-        if (K.c_nev) {  // lane (row, c) tiles always give this lane column c
-            const int col = lane % C;
+        if (K.c_nev) {  // lane (row, a) of every tile of the round works on column acol[a]
+            const int col = s_geo.acol[lane % s_geo.na];
             atomicAdd(&B.neval[col], K.c_nev);
             atomicAdd(&B.edges[col], K.c_edg);
             if (K.c_warn) atomicAdd(&B.warn[col], (unsigned long long)K.c_warn);
@@ -1438,6 +1219,8 @@ __global__ void __launch_bounds__(kLpThreads, DLP_LP_MINB) k_lp_fused(LPParams P
                     decide_actions_act(S, P, s_res, &s_claimed, 0);
                 else
                     decide_actions(S, P, s_res, &s_claimed, 0);
+                set_geo(s_geo, S.fr_mask | S.cert_mask, C, wsm - DLP_WIN_MAX, 32);
+                set_geo(s_geo_l, S.fr_mask | S.cert_mask, C, wsm - DLP_WIN_MAX, DLP_LONG_RPT);
             }
         }
         for (int j = 0; j < 3; j++) ncur[j] = s_cnt[j];
@@ -1532,11 +1315,8 @@ void lp_setup(Engine& E) {
     if (E.lp_grid) return;
     l2_setup(E);
     if (E.ncol > kMaxCols) throw CudaFailure(cudaErrorInvalidValue, "ncol > kMaxCols", __FILE__, __LINE__);
-    E.lp_smem = std::max((size_t)(kLpThreads / 32) * (kWin * (E.ncol + 1) + 32),
+    E.lp_smem = std::max((size_t)(kLpThreads / 32) * warp_smem_doubles(E.ncol),
                          (size_t)2 * kHubWin * (E.ncol + 1)) * sizeof(double);
-#ifdef DLP_PC
-    E.lp_smem = std::max(E.lp_smem, (size_t)4 * kPCSlots * pc_slot_bytes(E.ncol));
-#endif
     DLP_CUDA_TRY(cudaFuncSetAttribute(k_lp_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)E.lp_smem));
     if (const char* v = getenv("DLP_CARVEOUT"))  // shared-memory share of L1 (percent), tuning
         DLP_CUDA_TRY(cudaFuncSetAttribute(k_lp_fused, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(v)));
@@ -1547,6 +1327,7 @@ void lp_setup(Engine& E) {
     E.lp_grid = E.sm_count * occ;
     if (const char* g = getenv("DLP_LP_GRID")) E.lp_grid = atoi(g);
     E.lp_trace_path = getenv("DLP_LP_TRACE");
+    if (const char* v = getenv("DLP_CERT_HOLD")) E.lp_cert_hold = atoi(v);
     if (const char* v = getenv("DLP_LONG_ROW")) {
         int x = atoi(v);
         DLP_CUDA_TRY(cudaMemcpyToSymbol(c_long_row, &x, sizeof(int)));
@@ -1589,6 +1370,7 @@ void lp_run_dev(Engine& E, double delta, long long max_iter, bool itlp) {
     P.itlp = itlp ? 1 : 0;
     P.action_mode = 0;
     P.cleanup = 0;
+    P.cert_hold = E.lp_cert_hold;
     P.log_u = nullptr;
     P.log_em = P.log_chg = nullptr;
     DLP_CUDA_TRY(cudaMemsetAsync(E.ctl, 0, sizeof(LPCtl), E.st));
@@ -1651,6 +1433,7 @@ void lp_run_actions(Engine& E, double delta, bool first, bool cleanup) {
     P.itlp = 0;
     P.action_mode = 1;
     P.cleanup = cleanup ? 1 : 0;
+    P.cert_hold = 0;
     P.log_u = nullptr;
     P.log_em = P.log_chg = nullptr;
     const bool rows = E.shard_rows && E.shard_world > 1;

@@ -11,6 +11,9 @@ Mirrors the reference's engine surface (/root/reference/pkg/src/dynlp/):
 * ``apply_batch_structure`` engine.py:141-156
 * ``run_batches``       engine.py:416-423
 * ``itlp_batch_solve``  baselines.py:236-253
+* ``harmonic_solve`` / ``oracle_batch_solve`` / ``stlp_batch_solve``
+                        baselines.py:163-190, 321-371 (dense Cholesky on the
+                        device, cuSOLVER)
 
 Everything below the C-ABI (include/dynlp_b200.h) runs as sm_100a CUDA
 kernels; this module only marshals arguments and maps status codes onto the
@@ -22,6 +25,7 @@ from __future__ import annotations
 import ctypes as C
 import math
 import os
+import time
 from dataclasses import dataclass, field
 from typing import Optional, Union
 
@@ -36,6 +40,7 @@ MODE_GAUSS_SEIDEL = "sequential_gauss_seidel"
 DEFAULT_DELTA = 1e-4
 MAX_ITERATIONS_PER_VERTEX = 10
 UNLABELED = -1
+DENSE_SOLVE_CAP = 5000  # baselines.py:29
 
 
 @dataclass
@@ -262,6 +267,16 @@ class DynamicGraph:
         self._check(self._lib.dlp_write_labels(self._h, _native.ptr(f), n))
         self._version += 1
 
+    def harmonic(self, stlp: bool = False, dense_cap: int = DENSE_SOLVE_CAP):
+        """Closed-form harmonic labels on the device: (C, n) array and the
+        count of alive vertices pinned to 0.5 as unreachable."""
+        n = self.num_slots
+        f = np.empty((self.ncol, n), dtype=np.float64)
+        unr = np.zeros(1, dtype=np.int64)
+        self._check(self._lib.dlp_harmonic_solve(self._h, int(bool(stlp)), int(dense_cap), _native.ptr(f), n,
+                                                 _native.ptr(unr)))
+        return f, int(unr[0])
+
     def _check(self, rc):
         if rc != 0:
             _raise(self._lib, self._h, rc)
@@ -440,6 +455,48 @@ def run_batches(graph: DynamicGraph, labels: LabelState, batches, cfg: EngineCon
         nxt = batches[i + 1] if pipelined and i + 1 < len(batches) else None
         out.append(apply_batch(graph, labels, b, cfg, next_batch=nxt)[1])
     return out
+
+
+def harmonic_solve(graph: DynamicGraph, labels: LabelState, dense_cap: int = DENSE_SOLVE_CAP,
+                   return_info: bool = False):
+    """baselines.harmonic_solve (baselines.py:163-190) on the device: the
+    closed-form labels of the current graph, unreachable vertices at 0.5.
+    Binary engines return the (n,) vector, C-column engines (C, n)."""
+    labels._bind(graph)
+    f, unr = graph.harmonic(False, dense_cap)
+    out = f[0] if graph.ncol == 1 else f
+    return (out, {"unreachable_pinned": unr}) if return_info else out
+
+
+def _solve_batch(graph, labels, batch, stlp, dense_cap, method):
+    started = time.perf_counter()
+    apply_batch_structure(graph, labels, batch)
+    f, _ = graph.harmonic(stlp, dense_cap)
+    gt = labels.gt
+    unl = np.flatnonzero(graph.alive & (gt[: graph.num_slots] == UNLABELED))
+    cur = labels.F.copy()
+    cur[:, unl] = f[:, unl]
+    graph.write_labels(cur)
+    reps = []
+    for _ in range(graph.ncol):
+        r = IterationReport(method=method, t=int(batch.t), iterations=1, updates=len(unl), converged=True)
+        r.wall_time_ms = (time.perf_counter() - started) * 1000.0
+        reps.append(r)
+    return labels, _result(graph, reps)
+
+
+def oracle_batch_solve(graph: DynamicGraph, labels: LabelState, batch, cfg: EngineConfig,
+                       dense_cap: int = DENSE_SOLVE_CAP):
+    """baselines.oracle_batch_solve (baselines.py:346-371): structure, then the
+    closed-form solution of the whole graph."""
+    return _solve_batch(graph, labels, batch, False, dense_cap, "oracle")
+
+
+def stlp_batch_solve(graph: DynamicGraph, labels: LabelState, batch, cfg: EngineConfig,
+                     dense_cap: int = DENSE_SOLVE_CAP):
+    """baselines.stlp_batch_solve (baselines.py:321-343): structure, then the
+    short-circuit solve (same linear system; both classes must be present)."""
+    return _solve_batch(graph, labels, batch, True, dense_cap, "stlp")
 
 
 def itlp_batch_solve(graph: DynamicGraph, labels: LabelState, batch, cfg: EngineConfig):

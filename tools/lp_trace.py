@@ -66,6 +66,14 @@ def summarise(a):
             if sel.any():
                 print(f"      longest [{lo:.0f},{hi:.0f}): rounds {sel.sum()}, phase1 median {np.median(ph1[sel]):.1f} us, "
                       f"total {ph1[sel].sum() / 1e3:.2f} ms, ns per longest entry {np.median(ph1[sel] * 1e3 / ml[sel]):.1f}")
+    masks = a[:, 3].astype(np.int64)
+    fr_cols = np.array([bin(int(x) & 0xFFFF).count("1") for x in masks])
+    ce_cols = np.array([bin((int(x) >> 16) & 0xFFFF).count("1") for x in masks])
+    if ce.any():
+        print(f"  certify rounds by certifying columns: "
+              + ", ".join(f"{k}:{int((ce_cols == k).sum())}" for k in range(1, 17) if (ce_cols == k).any())
+              + f"; column-certifies total {int(ce_cols.sum())}")
+    print(f"  frontier columns per round: mean {fr_cols.mean():.2f}")
     if ce.any():
         print(f"  certify: us/round={dt[ce].mean():.1f} rows/round={rows[ce].mean():.0f} "
               f"long/round={nlong[ce].mean():.0f} hub/round={nhub[ce].mean():.0f}")
