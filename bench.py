@@ -54,6 +54,12 @@ CONFIGS = {
                fractions=(0.99, 0.01, 0.0), seed=0, delta=1e-4,
                desc="C2: synthetic blobs 1M x 128-dim, 10 classes (one-vs-rest columns), "
                     "cosine kNN k=10, 1% seeds, 100 insert batches of 10k"),
+    # C2 with binary labels (one label column): the single-column kernel path at 1M
+    # (diagnostic; the reference itself is binary)
+    "c2b": dict(n=1_000_000, dim=128, classes=2, k=10, seed_frac=0.01, batch=10_000,
+                fractions=(0.99, 0.01, 0.0), seed=0, delta=1e-4,
+                desc="C2 binary: synthetic blobs 1M x 128-dim, 2 classes (one label column), cosine kNN "
+                     "k=10, 1% seeds, 100 insert batches of 10k"),
     # configs[0]: 10k x 16, 3 classes, k=10, 1% seeds, batches of 500
     "c1": dict(n=10_000, dim=16, classes=3, k=10, seed_frac=0.01, batch=500,
                fractions=(0.99, 0.01, 0.0), seed=0, delta=1e-4,
@@ -64,6 +70,13 @@ CONFIGS = {
                fractions=(0.99, 0.01, 0.0), seed=1, delta=1e-4,
                desc="C4: synthetic blobs 10M x 64-dim, binary, cosine kNN k=16, 0.1% seeds, "
                     "insert batches of 100k (single GPU)"),
+    # configs[4] per SURVEY §8(d) D-2: 50M points uniform in the unit cube (one giant
+    # component), exact 3-D k-NN k=10, binary (class = x > 1/2), 0.1% seeds; the
+    # row-partitioned multi-GPU mode's workload (--shard-mode rows)
+    "c5": dict(n=50_000_000, dim=3, classes=2, k=10, seed_frac=0.001, batch=500_000,
+               fractions=(0.99, 0.01, 0.0), seed=2, delta=1e-4, gen="cube",
+               desc="C5: 50M points uniform in [0,1]^3, exact 3-D kNN k=10 (single giant component), "
+                    "binary, 0.1% seeds, insert batches of 500k"),
     # configs[2] per SURVEY §8(d) D-2: a 1.7M-point dataset; phase 1 = 100 insert batches
     # of 10k (|V| -> 1M, untimed), phase 2 = 100 mixed batches of 6.9k unlabeled + 0.1k
     # GT inserts + 3k deletes (|V| 1.0M -> 1.4M alive ... the timed tail)
@@ -100,6 +113,8 @@ def stream_key(cfg):
         "_" + "_".join(str(x) for x in cfg["fractions"])
     if cfg.get("boot_batches"):
         key += f"_b{cfg['boot_batches']}m{cfg['mixed_batches']}"
+    if cfg.get("gen"):
+        key += "_" + cfg["gen"]
     return key + "_knn64"
 
 
@@ -125,8 +140,12 @@ def make_stream(cfg, device):
     path = os.path.join(cache_dir, f"stream_{stream_key(cfg)}.npz")
     if not os.path.exists(path):
         t0 = time.time()
-        bl = streams.make_blobs(cfg["n"], cfg["dim"], cfg["classes"], cfg["seed"])
-        edges = streams.knn_graph_torch64(bl.x, cfg["k"], device=device or "cpu")
+        if cfg.get("gen") == "cube":
+            bl = streams.uniform_cube(cfg["n"], cfg["seed"])
+            edges = streams.knn_graph_grid3d(bl.x, cfg["k"])
+        else:
+            bl = streams.make_blobs(cfg["n"], cfg["dim"], cfg["classes"], cfg["seed"])
+            edges = streams.knn_graph_torch64(bl.x, cfg["k"], device=device or "cpu")
         gt = streams.stratified_seeds(bl.classes, cfg["seed_frac"], cfg["seed"])
         fi, fg, fd = cfg["fractions"]
         phases = None
@@ -698,7 +717,7 @@ def main():
                         "updates": sum(r.updates for r in repI),
                         "dynlp_ms_same_batch": repsA[0][0].wall_time_ms,
                         "speedup_dynlp_vs_itlp": wall_itlp / max(repsA[0][0].wall_time_ms, 1e-9)}
-    if rank == 0 and not args.no_knn:
+    if rank == 0 and not args.no_knn and not cfg.get("gen"):  # cosine k-NN leg (blob configs)
         line["knn"] = knn_leg(cfg, local, K)
     if rank == 0 and F0 is not None:
         cores = host_cores()

@@ -138,8 +138,18 @@ int dlp_shard_set(dlp_engine* e, int rank, int world);
  * through the same callback (isum segments) and each rank applies the others'
  * labels and frontier claims, so every rank holds the whole label matrix.
  * Must be chosen before the first batch. */
-enum { DLP_SHARD_COMPONENTS = 0, DLP_SHARD_ROWS = 1 };
+/* components: sticky LPT placement by edge count; rows:
+ * row partition for one giant component (E-3); components_hash: placement
+ * by a hash of the component's root (no balancing) */
+enum { DLP_SHARD_COMPONENTS = 0, DLP_SHARD_ROWS = 1, DLP_SHARD_COMPONENTS_HASH = 2 };
 int dlp_shard_mode(dlp_engine* e, int mode);
+/* NCCL communicator inside the handle: rank 0 creates the
+ * 128-byte id, the caller broadcasts it (torch.distributed), every rank
+ * attaches; dlp_apply_batch_sharded with reduce = NULL then runs every
+ * exchange as an NCCL collective on device buffers on the engine's stream
+ * (phase all-reduces, label migration max-reduce, row all-gather). */
+int dlp_nccl_unique_id(void* id);
+int dlp_shard_nccl(dlp_engine* e, const void* id, int world, int rank);
 int dlp_apply_batch_sharded(dlp_engine* e, const dlp_config* cfg, const dlp_batch* batch, dlp_allreduce_fn reduce,
                             void* ctx, dlp_report* reports);
 int dlp_read_owned(dlp_engine* e, uint8_t* owned, int64_t n);

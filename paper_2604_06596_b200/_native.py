@@ -58,6 +58,8 @@ SIGNATURES = {
     "dlp_apply_structure": (_int, [_p, _p]),
     "dlp_itlp_batch": (_int, [_p, _p, _p, _p]),
     "dlp_reserve": (_int, [_p, _i64, _i64]),
+    "dlp_nccl_unique_id": (_int, [_p]),
+    "dlp_shard_nccl": (_int, [_p, _p, _int, _int]),
     "dlp_shard_set": (_int, [_p, _int, _int]),
     "dlp_shard_mode": (_int, [_p, _int]),
     "dlp_apply_batch_sharded": (_int, [_p, _p, _p, _p, _p, _p]),
@@ -110,6 +112,8 @@ def load(build_if_missing: bool = False):
                     "(the B200 engine has no CPU fallback)")
         lib = C.CDLL(LIB_PATH)
         for name, (res, args) in SIGNATURES.items():
+            if os.environ.get("DLP_LIB_PATH") and not hasattr(lib, name):
+                continue  # an older tuning variant (A/B runs) may lack newer entry points
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args

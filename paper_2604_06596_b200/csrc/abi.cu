@@ -49,6 +49,12 @@ int fail(Engine& E, int code, const char* fmt, ...) {
     return code;
 }
 
+// a failed reduction: the engine's NCCL path leaves its reason in E.err
+int coll_fail(Engine& E) {
+    if (E.nccl && !E.err.empty()) return fail(E, DLP_EINTERNAL, "collective failed: %s", E.err.c_str());
+    return fail(E, DLP_EINTERNAL, "collective failed");
+}
+
 int cuda_fail(dlp_engine* h, const CudaFailure& f) {
     h->poisoned = true;
     return fail(h->E, DLP_ECUDA, "CUDA error %s at %s:%d (%s)", cudaGetErrorString(f.err), f.file, f.line, f.expr);
@@ -308,7 +314,7 @@ int rows_exchange(Engine& E, dlp_allreduce_fn reduce, void* rctx) {
     std::vector<int64_t> cnt(W, 0), z(1, 0);
     std::vector<double> zd(1, 0.0);
     cnt[me] = (int64_t)keep.size();
-    if (reduce(rctx, z.data(), 1, cnt.data(), W, zd.data(), 1)) return fail(E, DLP_EINTERNAL, "collective failed");
+    if (reduce(rctx, z.data(), 1, cnt.data(), W, zd.data(), 1)) return coll_fail(E);
     long long tot = 0, off = 0;
     for (int r = 0; r < W; r++) {
         if (r == me) off = tot;
@@ -326,7 +332,7 @@ int rows_exchange(Engine& E, dlp_allreduce_fn reduce, void* rctx) {
     }
     if (buf.size() > (size_t)INT32_MAX) return fail(E, DLP_EINTERNAL, "row exchange too large");
     if (reduce(rctx, z.data(), 1, buf.data(), (int32_t)buf.size(), zd.data(), 1))
-        return fail(E, DLP_EINTERNAL, "collective failed");
+        return coll_fail(E);
     const long long m = tot - cnt[me];
     if (m == 0) return DLP_OK;
     std::vector<int> ru(m);
@@ -356,6 +362,49 @@ int rows_exchange(Engine& E, dlp_allreduce_fn reduce, void* rctx) {
     return DLP_OK;
 }
 
+// Row partition over NCCL: the round's evaluated rows are packed on the
+// device (record = vertex, evaluated mask, changed mask, C label words), the
+// per-rank counts and then the records (padded to the largest count) are
+// all-gathered device to device, and the other ranks' records are unpacked
+// into the k_rows_apply inputs on the device.  One small D2H (the counts).
+int rows_exchange_nccl(Engine& E) {
+    const int C = E.ncol, W = E.shard_world, me = E.shard_rank;
+    LPCtl& L = *E.h_ctl.p;
+    const long long n = L.log_n;
+    const int rec = 3 + C;
+    E.rows_send.reserve((size_t)(n + 1) * rec, 0, E.st);
+    E.comm_buf.reserve(2 * (size_t)W + 2, 0, E.st);
+    unsigned long long* cnt_d = E.comm_buf.p;  // [0]: own count, [W..2W): gathered counts
+    DLP_CUDA_TRY(cudaMemsetAsync(cnt_d, 0, 8, E.st));
+    rows_pack(E, n, E.rows_send.p, cnt_d);
+    if (nccl_allgather_u64(E, cnt_d, cnt_d + W, 1)) return fail(E, DLP_EINTERNAL, "%s", E.err.c_str());
+    std::vector<unsigned long long> cnt(W);
+    DLP_CUDA_TRY(cudaMemcpyAsync(cnt.data(), cnt_d + W, W * 8, cudaMemcpyDeviceToHost, E.st));
+    DLP_CUDA_TRY(cudaStreamSynchronize(E.st));
+    unsigned long long mx = 0, tot = 0;
+    for (int r = 0; r < W; r++) {
+        mx = std::max(mx, cnt[r]);
+        tot += cnt[r];
+    }
+    const long long m = (long long)(tot - cnt[me]);
+    if (mx == 0) return DLP_OK;
+    E.rows_recv.reserve((size_t)W * mx * rec, 0, E.st);
+    if (nccl_allgather_u64(E, E.rows_send.p, E.rows_recv.p, (size_t)mx * rec))
+        return fail(E, DLP_EINTERNAL, "%s", E.err.c_str());
+    if (m == 0) return DLP_OK;
+    E.rx_u.reserve(m, 0, E.st);
+    E.rx_em.reserve(m, 0, E.st);
+    E.rx_chg.reserve(m, 0, E.st);
+    E.rx_val.reserve((size_t)m * C, 0, E.st);
+    std::vector<long long> base(W + 1, 0);  // output offset of each rank's records (own skipped)
+    for (int r = 0; r < W; r++) base[r + 1] = base[r] + (r == me ? 0 : (long long)cnt[r]);
+    rows_unpack(E, W, me, (long long)mx, cnt, base, E.rows_recv.p);
+    lp_rows_apply(E, m, L.r_par);
+    DLP_CUDA_TRY(cudaMemcpyAsync(L.has_fr, E.ctl->has_fr, sizeof(L.has_fr), cudaMemcpyDeviceToHost, E.st));
+    DLP_CUDA_TRY(cudaStreamSynchronize(E.st));
+    return DLP_OK;
+}
+
 int sharded_lp(Engine& E, const dlp_config* cfg, long long max_iter, dlp_allreduce_fn reduce, void* rctx,
                std::vector<ColCtl>& col, double* lp_ms, long long* launches) {
     const int C = E.ncol;
@@ -366,9 +415,16 @@ int sharded_lp(Engine& E, const dlp_config* cfg, long long max_iter, dlp_allredu
         long long m = migr_collect(E, E.n_slots);
         std::vector<int64_t> mi(1, m), ms(1, 0);
         std::vector<double> md(1, 0.0);
-        if (reduce(rctx, mi.data(), 1, ms.data(), 1, md.data(), 1)) return fail(E, DLP_EINTERNAL, "collective failed");
+        if (reduce(rctx, mi.data(), 1, ms.data(), 1, md.data(), 1)) return coll_fail(E);
         if (mi[0] != m) return fail(E, DLP_EINTERNAL, "shards disagree on migrated vertices");
-        if (m) {
+        if (m && reduce == nccl_reduce) {  // device-resident max-reduction
+            const size_t cnt = (size_t)m * C;
+            E.migr_buf.reserve(cnt, 0, E.st);
+            migr_pack(E, m, E.migr_buf.p);
+            if (nccl_max_f64(E, E.migr_buf.p, cnt)) return fail(E, DLP_EINTERNAL, "%s", E.err.c_str());
+            migr_unpack(E, m, E.migr_buf.p);
+            DLP_CUDA_TRY(cudaStreamSynchronize(E.st));
+        } else if (m) {
             const size_t cnt = (size_t)m * C;
             E.migr_buf.reserve(cnt, 0, E.st);
             std::vector<double> hb(cnt);
@@ -377,7 +433,7 @@ int sharded_lp(Engine& E, const dlp_config* cfg, long long max_iter, dlp_allredu
             DLP_CUDA_TRY(cudaStreamSynchronize(E.st));
             std::vector<int64_t> z1(1, 0), z2(1, 0);
             if (reduce(rctx, z1.data(), 1, z2.data(), 1, hb.data(), (int32_t)cnt))
-                return fail(E, DLP_EINTERNAL, "collective failed");
+                return coll_fail(E);
             DLP_CUDA_TRY(cudaMemcpyAsync(E.migr_buf.p, hb.data(), cnt * 8, cudaMemcpyHostToDevice, E.st));
             migr_unpack(E, m, E.migr_buf.p);
             DLP_CUDA_TRY(cudaStreamSynchronize(E.st));
@@ -389,7 +445,7 @@ int sharded_lp(Engine& E, const dlp_config* cfg, long long max_iter, dlp_allredu
     DLP_CUDA_TRY(cudaStreamSynchronize(E.st));
     isum[0] = E.h_ds.p->n_f0;
     isum[1] = E.h_ds.p->n_elist;
-    if (reduce(rctx, imax.data(), 1, isum.data(), 2, dmax.data(), 1)) return fail(E, DLP_EINTERNAL, "collective failed");
+    if (reduce(rctx, imax.data(), 1, isum.data(), 2, dmax.data(), 1)) return coll_fail(E);
     std::vector<long long> elig_g(C, isum[1]);
     for (auto& c : col) c.has_fr = isum[0] > 0;
     bool first = true;
@@ -434,7 +490,7 @@ int sharded_lp(Engine& E, const dlp_config* cfg, long long max_iter, dlp_allredu
         DLP_CUDA_TRY(cudaMemcpyAsync(E.h_ctl.p, E.ctl, sizeof(LPCtl), cudaMemcpyDeviceToHost, E.st));
         DLP_CUDA_TRY(cudaStreamSynchronize(E.st));
         if (rows) {
-            int rc = rows_exchange(E, reduce, rctx);
+            int rc = reduce == nccl_reduce ? rows_exchange_nccl(E) : rows_exchange(E, reduce, rctx);
             if (rc) return rc;
         }
         const LPCtl& L = *E.h_ctl.p;
@@ -451,14 +507,14 @@ int sharded_lp(Engine& E, const dlp_config* cfg, long long max_iter, dlp_allredu
             dm[c] = col[c].act == ACT_CERTIFY ? L.ph_mc[c] : 0.0;
         }
         if (reduce(rctx, rmaxv.data(), C, sums.data(), 5 * C, dm.data(), C))
-            return fail(E, DLP_EINTERNAL, "collective failed");
+            return coll_fail(E);
         // the frontier phase's max_change is its last global round's: shards that
         // ran fewer rounds had an empty frontier in that round
         std::vector<int64_t> none(1, 0), nsum(1, 0);
         std::vector<double> mc(C, -1.0);
         for (int c = 0; c < C; c++)
             if (col[c].act == ACT_FRONTIER && L.ph_rounds[c] == rmaxv[c] && rmaxv[c] > 0) mc[c] = L.ph_mc[c];
-        if (reduce(rctx, none.data(), 1, nsum.data(), 1, mc.data(), C)) return fail(E, DLP_EINTERNAL, "collective failed");
+        if (reduce(rctx, none.data(), 1, nsum.data(), 1, mc.data(), C)) return coll_fail(E);
         for (int c = 0; c < C; c++) {
             ColCtl& k = col[c];
             elig_g[c] = sums[4 * C + c];
@@ -591,6 +647,7 @@ int run_batch(dlp_engine* h, const dlp_config* cfg, const dlp_batch* batch, bool
         }
         host_mark(E, "staged");
         long long launches0 = E.launches;
+        E.view_seq++;  // LP view cache: changes of this batch get this sequence number
         k_reset_batch<<<1, 1, 0, E.st>>>(E.ds);
         E.launches++;
         apply_deletes_dev(E, bd);
@@ -799,17 +856,44 @@ int dlp_shard_set(dlp_engine* h, int rank, int world) {
 int dlp_shard_mode(dlp_engine* h, int mode) {
     if (!h) return DLP_EINTERNAL;
     Engine& E = h->E;
-    if (mode != DLP_SHARD_COMPONENTS && mode != DLP_SHARD_ROWS) return fail(E, DLP_EVALIDATION, "bad shard mode");
-    if (E.n_slots != 0 && mode != E.shard_rows)
+    if (mode != DLP_SHARD_COMPONENTS && mode != DLP_SHARD_ROWS && mode != DLP_SHARD_COMPONENTS_HASH)
+        return fail(E, DLP_EVALIDATION, "bad shard mode");
+    const int rows = mode == DLP_SHARD_ROWS ? 1 : 0, lpt = mode == DLP_SHARD_COMPONENTS ? 1 : 0;
+    if (E.n_slots != 0 && (rows != E.shard_rows || lpt != E.shard_lpt))
         return fail(E, DLP_EVALIDATION, "the shard mode must be chosen before the first batch");
-    E.shard_rows = mode;
+    E.shard_rows = rows;
+    E.shard_lpt = lpt;
+    return DLP_OK;
+}
+
+int dlp_nccl_unique_id(void* id) {
+    std::string err;
+    return nccl_unique_id(id, &err);
+}
+
+int dlp_shard_nccl(dlp_engine* h, const void* id, int world, int rank) {
+    Engine& E = h->E;
+    if (world < 1 || rank < 0 || rank >= world) return fail(E, DLP_EVALIDATION, "bad rank %d / world %d", rank, world);
+    if (world > 255) return fail(E, DLP_EVALIDATION, "world > 255 is not supported");
+    try {
+        DLP_CUDA_TRY(cudaSetDevice(E.device));
+        nccl_detach(E);
+        int rc = nccl_attach(E, id, world, rank);
+        if (rc) return fail(E, rc, "%s", E.err.c_str());
+    } catch (const CudaFailure& f) {
+        return cuda_fail(h, f);
+    }
     return DLP_OK;
 }
 
 int dlp_apply_batch_sharded(dlp_engine* h, const dlp_config* cfg, const dlp_batch* batch, dlp_allreduce_fn reduce,
                             void* ctx, dlp_report* reports) {
     if (!h) return DLP_EINTERNAL;
-    if (!reduce) return fail(h->E, DLP_EVALIDATION, "a reduction callback is required");
+    if (!reduce) {  // the engine's own NCCL communicator (dlp_shard_nccl)
+        if (!h->E.nccl) return fail(h->E, DLP_EVALIDATION, "a reduction callback or an NCCL communicator is required");
+        reduce = nccl_reduce;
+        ctx = &h->E;
+    }
     return run_batch(h, cfg, batch, false, false, reports, KIND_DYNLP, reduce, ctx);
 }
 
@@ -856,6 +940,10 @@ int dlp_destroy(dlp_engine* h) {
     cudaStreamSynchronize(E.st);
     if (E.l2_persist) cudaCtxResetPersistingL2Cache();  // hand the carve-out's lines back
     if (E.cusolver) cusolverDnDestroy((cusolverDnHandle_t)E.cusolver);
+    nccl_detach(E);
+    E.comm_buf.release();
+    E.rows_send.release();
+    E.rows_recv.release();
     DevArray<unsigned char>* u8s[] = {&E.alive, &E.mark, &E.root_gt, &E.owner_rank, &E.migr_from, &E.d_stage,
                                       &E.cub_tmp, &E.cc_hit_root, &E.cc_hit};
     E.migr_flag.release();
@@ -864,6 +952,12 @@ int dlp_destroy(dlp_engine* h) {
     E.migr_buf.release();
     for (auto* a : u8s) a->release();
     E.purge_flag.release();
+    E.vlen.release();
+    E.row_mod.release();
+    E.view_b.release();
+    E.view_st.release();
+    E.wsum.release();
+    E.q01.release();
     E.gt.release();
     E.row_start.release();
     DevArray<int>* i32s[] = {&E.row_len, &E.row_up, &E.row_cap, &E.parent, &E.cnt_up, &E.cnt_dn, &E.grp_start,

@@ -236,15 +236,24 @@ __device__ inline unsigned int ld_acquire_u32(const unsigned int* p) {
 
 // Grid-wide barrier for a cooperatively launched (co-resident) grid: a
 // monotone arrival counter, one atomic per CTA, acquire-spin by one thread.
+// The spin reads with ld.relaxed (an ld.acquire per iteration would
+// invalidate the SM's L1 -- CCTL.IVALL -- under the CTAs still working on
+// that SM); one fence after the exit gives the acquire.
+__device__ inline unsigned int ld_relaxed_u32(const unsigned int* p) {
+    unsigned int v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
 __device__ inline void grid_sync(unsigned int* ctr, unsigned int& target) {
     __syncthreads();
     if (threadIdx.x == 0) {
         target += gridDim.x;
         __threadfence();
         atomicAdd(ctr, 1u);
-        while (ld_acquire_u32(ctr) < target) {
+        while (ld_relaxed_u32(ctr) < target) {
+            __nanosleep(32);
         }
-
         __threadfence();
     }
     __syncthreads();

@@ -23,6 +23,7 @@
 #pragma once
 
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "common.cuh"
@@ -179,6 +180,11 @@ struct Engine {
     long long intra_k = 0;
     bool cc_valid = true;  // global union-find consistent with the live graph
     int shard_rank = 0, shard_world = 1;  // component sharding (dlp_shard_set)
+    int shard_lpt = 1;   // component placement: 1 = sticky LPT by edge count, 0 = hash of the root
+    std::unordered_map<long long, unsigned char> place;  // root -> rank of the last placement
+    DevArray<unsigned long long> comp_w, comp_wl;
+    DevArray<long long> comp_roots;
+    DevArray<unsigned char> comp_own, root_owner;
     int shard_rows = 0;  // 1: row partition (dlp_shard_mode): vertex v is owned by rank v % world
     // row partition: per-round work-item log (vertex, evaluated mask, changed
     // mask; the values are the compact staging Y) and remote rows to apply
@@ -188,7 +194,13 @@ struct Engine {
 
     // per-vertex ----------------------------------------------------------
     DevArray<unsigned char> alive, mark, root_gt, owner_rank, migr_from;
-    DevArray<unsigned char> cc_hit_root, cc_hit;  // decremental connectivity: hit roots / members
+    DevArray<unsigned char> cc_hit_root, cc_hit;
+    DevArray<int> vlen;            // LP view: unlabeled neighbours per row (pool: nbr_sp / wgt_sp)
+    DevArray<int> row_mod, view_b; // batch sequence of a row's last change / of its view's build
+    DevArray<long long> view_st;   // row_start the view was built at
+    int view_seq = 1;              // batch sequence number (advanced per batch with structure)
+    int view_inval = 0;            // views built before this sequence are invalid (pool repacked)
+    DevArray<double> wsum, q01;    // LP view row constants: w_all; (w0, w1) / w_all per column  // decremental connectivity: hit roots / members
     DevArray<int> migr_flag, migr_pos, migr_list;
     DevArray<double> migr_buf;
     DevArray<int> purge_flag;
@@ -235,7 +247,9 @@ struct Engine {
     LPCtl* ctl = nullptr;
     PinnedArray<LPCtl> h_ctl;
     int lp_grid = 0;
-    void* cusolver = nullptr;  // cusolverDnHandle_t of the harmonic oracle (created on first use)
+    void* cusolver = nullptr;
+    void* nccl = nullptr;      // ncclComm_t of a sharded engine (dlp_shard_nccl), else null
+    DevArray<unsigned long long> comm_buf, rows_send, rows_recv;  // NCCL staging (device)  // cusolverDnHandle_t of the harmonic oracle (created on first use)
     int lp_cert_hold = 1 << 30;  // certify alignment: max rounds a certify waits (DLP_CERT_HOLD)
     int l2_mode = 1;            // label L2 residency: 0 none, 1 persisting carve-out, 2 + access window
     size_t l2_persist = 0;      // persisting L2 carve-out (bytes)
@@ -276,6 +290,17 @@ void lp_run_actions(Engine& E, double delta, bool first, bool cleanup);
 void lp_rows_apply(Engine& E, long long m, long long r_par);
 void lp_setup(Engine& E);
 void lp_dump_trace(Engine& E, long long rounds);
+// NCCL inside the handle (comm.cu)
+int nccl_unique_id(void* out, std::string* err);
+int nccl_attach(Engine& E, const void* id, int world, int rank);
+void nccl_detach(Engine& E);
+int nccl_reduce(void* ctx, int64_t* imax, int32_t nimax, int64_t* isum, int32_t nisum, double* dmax, int32_t ndmax);
+int nccl_max_f64(Engine& E, double* d, size_t n);
+int nccl_allgather_u64(Engine& E, const unsigned long long* send, unsigned long long* recv, size_t count);
+// row-partition record packing on the device (lp.cu)
+void rows_pack(Engine& E, long long n, unsigned long long* send, unsigned long long* count);
+void rows_unpack(Engine& E, int W, int me, long long mx, const std::vector<unsigned long long>& cnt,
+                 const std::vector<long long>& base, const unsigned long long* recv);
 // closed-form harmonic labels (harmonic.cu); out_host = C x n_slots
 int harmonic_solve_dev(Engine& E, int stlp, long long dense_cap, double* out_host, long long* fallback,
                        std::string* msg);

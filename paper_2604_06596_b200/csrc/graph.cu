@@ -73,6 +73,12 @@ void ensure_vertex_capacity(Engine& E, long long want) {
     E.elist_l.reserve(nc + 1, 0, st);
     E.elist_h.reserve(nc + 1, 0, st);
     grow_zero(E.eligm, nc, keep, st);
+    grow_zero(E.row_mod, nc, keep, st);
+    grow_zero(E.view_b, nc, keep, st);
+    grow_zero(E.view_st, nc, keep, st);
+    E.vlen.reserve(nc + 1, keep, st);
+    E.wsum.reserve(nc + 1, keep, st);
+    E.q01.reserve((size_t)(nc + 1) * E.ncol * 2, (size_t)keep * E.ncol * 2, st);
     grow_zero(E.emask_store, nc, keep, st);
     E.f0.reserve(nc + 1, 0, st);
     E.elist.reserve(nc + 1, 0, st);
@@ -576,6 +582,7 @@ void compact_pool(Engine& E, long long min_free) {
     }
     std::swap(E.nbr, E.nbr_sp);
     std::swap(E.wgt, E.wgt_sp);
+    E.view_inval = E.view_seq - 1;  // the LP view lived in the pool the repack just wrote
     // the new spare must match the pool's capacity for the next compaction
     E.nbr_sp.reserve(E.nbr.n, 0, st);
     E.wgt_sp.reserve(E.wgt.n, 0, st);
@@ -967,7 +974,7 @@ __global__ void k_eligible(long long n, int ncol, long long cap, const unsigned 
                            const int* par, const unsigned char* root_gt, const int* row_len, unsigned char* mark,
                            unsigned int* eligm, double* f0, double* f1, int* elist, int* f0list, DevState* ds,
                            int rank, int world, int rows, unsigned char* owner_rank, unsigned char* migr_from,
-                           int* migr_flag) {
+                           int* migr_flag, const unsigned char* root_owner, int* row_mod, int seq) {
     unsigned int allc = ncol >= 32 ? 0xffffffffu : ((1u << ncol) - 1u);
     long long iso = 0, unr = 0;
     for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < n; v += (long long)gridDim.x * blockDim.x) {
@@ -980,7 +987,7 @@ __global__ void k_eligible(long long n, int ncol, long long cap, const unsigned 
         } else if (world > 1) {  // sharded: only this rank's components are propagated here
             int mig = 0;
             if (e) {
-                int o = shard_owner(par[v], world);
+                int o = root_owner ? (int)root_owner[par[v]] : shard_owner(par[v], world);
                 int prev = owner_rank[v];
                 if (o != prev) {  // component moved: its label lives on rank `prev`
                     mig = 1;
@@ -1006,6 +1013,7 @@ __global__ void k_eligible(long long n, int ncol, long long cap, const unsigned 
             append_agg(elist, &ds->n_elist, (int)v);
             if (mark[v]) append_agg(f0list, &ds->n_f0, (int)v);
         }
+        if (mark[v]) row_mod[v] = seq;  // the row changed this batch: its LP view is stale
         mark[v] = 0;
     }
     iso = warp_sum(iso);
@@ -1014,6 +1022,109 @@ __global__ void k_eligible(long long n, int ncol, long long cap, const unsigned 
         atomicAdd((unsigned long long*)&ds->isolated, (unsigned long long)iso);
         atomicAdd((unsigned long long*)&ds->unreach, (unsigned long long)unr);
     }
+}
+
+// ---------------------------------------------------------------------------
+// Component placement for sharded batches: LPT
+// bin-packing by edge count, sticky across batches.  Every rank holds the
+// same structure, so every rank computes the same placement: components keep
+// the rank they had (by their root's last placement) unless the load
+// imbalance exceeds 25%, new components go to the least-loaded rank in
+// decreasing size order (ties: lowest root, lowest rank).  Moves are handled
+// by the existing label migration (owner_rank / migr_* per vertex).
+// ---------------------------------------------------------------------------
+__global__ void k_comp_weight(long long n, const unsigned char* alive, const int* par, const int* row_len,
+                              unsigned long long* cw) {
+    for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < n; v += (long long)gridDim.x * blockDim.x)
+        if (alive[v]) atomicAdd(&cw[par[v]], (unsigned long long)row_len[v] + 1ULL);
+}
+
+__global__ void k_comp_roots(long long n, const unsigned char* alive, const int* par, int* flag) {
+    for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < n; v += (long long)gridDim.x * blockDim.x)
+        flag[v] = (alive[v] && par[v] == (int)v) ? 1 : 0;
+}
+
+__global__ void k_comp_gather(long long n, const int* flag, const int* pos, const unsigned long long* cw,
+                              long long* roots, unsigned long long* w) {
+    for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < n; v += (long long)gridDim.x * blockDim.x)
+        if (flag[v]) {
+            roots[pos[v]] = v;
+            w[pos[v]] = cw[v];
+        }
+}
+
+__global__ void k_comp_place(long long m, const long long* roots, const unsigned char* own, unsigned char* root_owner) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m; i += (long long)gridDim.x * blockDim.x)
+        root_owner[roots[i]] = own[i];
+}
+
+const unsigned char* assign_components(Engine& E, long long n) {
+    cudaStream_t st = E.st;
+    const int W = E.shard_world;
+    E.comp_w.reserve(E.cap_n + 1, 0, st);
+    E.root_owner.reserve(E.cap_n + 1, 0, st);
+    DLP_CUDA_TRY(cudaMemsetAsync(E.comp_w.p, 0, n * sizeof(unsigned long long), st));
+    E.flag_i.reserve(n + 1, 0, st);
+    E.pos_i.reserve(n + 1, 0, st);
+    k_comp_weight<<<grid_for(n), kBlock, 0, st>>>(n, E.alive.p, E.parent.p, E.row_len.p, E.comp_w.p);
+    k_comp_roots<<<grid_for(n), kBlock, 0, st>>>(n, E.alive.p, E.parent.p, E.flag_i.p);
+    cub_scan(E, E.flag_i.p, E.pos_i.p, n);
+    int lp = 0, lf = 0;
+    DLP_CUDA_TRY(cudaMemcpyAsync(&lp, E.pos_i.p + n - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+    DLP_CUDA_TRY(cudaMemcpyAsync(&lf, E.flag_i.p + n - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+    DLP_CUDA_TRY(cudaStreamSynchronize(st));
+    const long long m = (long long)lp + lf;
+    E.launches += 3;
+    if (m == 0) return E.root_owner.p;
+    E.comp_roots.reserve(m + 1, 0, st);
+    E.comp_wl.reserve(m + 1, 0, st);
+    E.comp_own.reserve(m + 1, 0, st);
+    k_comp_gather<<<grid_for(n), kBlock, 0, st>>>(n, E.flag_i.p, E.pos_i.p, E.comp_w.p, E.comp_roots.p, E.comp_wl.p);
+    std::vector<long long> roots(m);
+    std::vector<unsigned long long> w(m);
+    DLP_CUDA_TRY(cudaMemcpyAsync(roots.data(), E.comp_roots.p, m * 8, cudaMemcpyDeviceToHost, st));
+    DLP_CUDA_TRY(cudaMemcpyAsync(w.data(), E.comp_wl.p, m * 8, cudaMemcpyDeviceToHost, st));
+    DLP_CUDA_TRY(cudaStreamSynchronize(st));
+    // placement (host, deterministic, identical on every rank)
+    std::vector<unsigned char> own(m, 0);
+    std::vector<unsigned long long> load(W, 0);
+    unsigned long long total = 0;
+    for (long long i = 0; i < m; i++) total += w[i];
+    std::vector<long long> fresh;
+    for (long long i = 0; i < m; i++) {
+        auto it = E.place.find(roots[i]);
+        if (it != E.place.end()) {
+            own[i] = it->second;
+            load[own[i]] += w[i];
+        } else {
+            fresh.push_back(i);
+        }
+    }
+    const unsigned long long avg = (total + W - 1) / W;
+    unsigned long long mx = 0;
+    for (int r = 0; r < W; r++) mx = std::max(mx, load[r]);
+    if (mx > avg + avg / 4) {  // imbalanced: full LPT
+        fresh.clear();
+        for (long long i = 0; i < m; i++) fresh.push_back(i);
+        std::fill(load.begin(), load.end(), 0ULL);
+    }
+    std::sort(fresh.begin(), fresh.end(), [&](long long a, long long b) {
+        return w[a] != w[b] ? w[a] > w[b] : roots[a] < roots[b];
+    });
+    for (long long i : fresh) {
+        int best = 0;
+        for (int r = 1; r < W; r++)
+            if (load[r] < load[best]) best = r;
+        own[i] = (unsigned char)best;
+        load[best] += w[i];
+    }
+    E.place.clear();
+    for (long long i = 0; i < m; i++) E.place.emplace(roots[i], own[i]);
+    DLP_CUDA_TRY(cudaMemcpyAsync(E.comp_own.p, own.data(), m, cudaMemcpyHostToDevice, st));
+    k_comp_place<<<grid_for(m), kBlock, 0, st>>>(m, E.comp_roots.p, E.comp_own.p, E.root_owner.p);
+    DLP_CUDA_TRY(cudaStreamSynchronize(st));  // own is a host temporary
+    E.launches += 2;
+    return E.root_owner.p;
 }
 
 void reach_and_pin_dev(Engine& E, int cc, long long n, const long long* dels, long long nd) {
@@ -1051,10 +1162,12 @@ void reach_and_pin_dev(Engine& E, int cc, long long n, const long long* dels, lo
     E.launches++;
     k_uf_flatten_root_gt<<<grid_for(n), kBlock, 0, st>>>(E.parent.p, n, E.alive.p, E.gt.p, E.root_gt.p);
     E.launches++;
+    const unsigned char* root_owner = nullptr;
+    if (E.shard_world > 1 && !E.shard_rows && E.shard_lpt) root_owner = assign_components(E, n);
     k_eligible<<<grid_for(n), kBlock, 0, st>>>(n, E.ncol, E.cap_n, E.alive.p, E.gt.p, E.parent.p, E.root_gt.p,
                                                E.row_len.p, E.mark.p, E.eligm.p, E.f[0].p, E.f[1].p, E.elist.p, E.f0.p,
                                                E.ds, E.shard_rank, E.shard_world, E.shard_rows, E.owner_rank.p, E.migr_from.p,
-                                               E.migr_flag.p);
+                                               E.migr_flag.p, root_owner, E.row_mod.p, E.view_seq);
     E.launches++;
 }
 

@@ -56,14 +56,20 @@ constexpr int kLpThreads = 256;
 #ifndef DLP_WIN
 #define DLP_WIN 32
 #endif
-#ifndef DLP_WIN_MAX
-#define DLP_WIN_MAX 64  // window slots per warp tile (span-1 rounds; C-wide rounds fit kWin)
+#ifndef DLP_LONG_RPT
+#define DLP_LONG_RPT 1  // rows per long-row tile (length imbalance wastes windows when > 1)
+#endif
+#ifndef DLP_SM_MAX_NA
+#define DLP_SM_MAX_NA 0  // rounds with at most this many active columns use step-major tiles (measured slower: off)
+#endif
+#ifndef DLP_LABEL_WIN
+#define DLP_LABEL_WIN 48  // C-wide label rows staged per warp window
 #endif
 #ifndef DLP_HUB_WIN
 #define DLP_HUB_WIN 128
 #endif
 #ifndef DLP_LP_MINB
-#define DLP_LP_MINB 3
+#define DLP_LP_MINB 2
 #endif
 #ifndef DLP_ACC_UNROLL
 #define DLP_ACC_UNROLL 4
@@ -99,9 +105,16 @@ __device__ inline int elig_class(unsigned int e) { return (int)((e >> kClassShif
 
 struct LPParams {
     const long long* row_start;
-    const int* row_len;
+    const int* row_len;  // full row length (edges_traversed)
     const int* nbr;
     const double* w;
+    // LP view (k_lp_view): unlabeled neighbours at the row's offset, their
+    // count, and the row constants w_all and (w0 / w_all, w1 / w_all) per column
+    const int* vnbr;
+    const double* vw;
+    const int* vlen;
+    const double* wsum;
+    const double* q01;
     double* X;  // canonical labels [v*C + c]
     double* Y;  // compact staging: [i*C + c] for work item i of the round
     unsigned int* eligm;
@@ -198,38 +211,45 @@ __device__ inline void append_u32(int* list, unsigned int* count, int v) {
     list[base + g.thread_rank()] = v;
 }
 
-struct ClaimCtx {
+// Where a round's claims go (the same for every thread of a round: kept in
+// shared memory, not in each thread's registers).
+struct ClaimTargets {
     unsigned int* fm_next;
     int* next[3];
     unsigned int* cnt;  // [3]
     const unsigned int* eligm;
-    const int* row_len;
+};
+
+struct ClaimCtx {
+    const ClaimTargets* t;
     unsigned int claimed;  // per-thread OR of claimed column bits
     // per-lane round counters of the lane's label column (flushed once per round)
-    unsigned long long c_nev, c_edg;
-    unsigned int c_warn;
+    unsigned int c_nev, c_warn;
+    unsigned long long c_edg;
     double c_rmax;
+    __device__ inline unsigned int* fm_next() const { return t->fm_next; }
 };
 
 // append-mode claim: add v (for the columns in `bits` where it is eligible)
 // to the next union frontier; the first claimer appends it to its class list
 __device__ inline void claim(ClaimCtx& k, int v, unsigned int bits) {
-    const unsigned int e = k.eligm[v];
+    const ClaimTargets& t = *k.t;
+    const unsigned int e = t.eligm[v];
     bits &= e;
     if (!bits) return;
     k.claimed |= bits;
-    unsigned int* fm = k.fm_next + v;
+    unsigned int* fm = t.fm_next + v;
     unsigned int cur = *(volatile unsigned int*)fm;
     if ((cur & bits) == bits) return;
     unsigned int old = atomicOr(fm, bits);
     if (old != 0) return;
     const int cls = elig_class(e);
     if (cls == CLS_SHORT)
-        append_u32(k.next[0], &k.cnt[0], v);
+        append_u32(t.next[0], &t.cnt[0], v);
     else if (cls == CLS_LONG)
-        append_u32(k.next[1], &k.cnt[1], v);
+        append_u32(t.next[1], &t.cnt[1], v);
     else
-        append_u32(k.next[2], &k.cnt[2], v);
+        append_u32(t.next[2], &t.cnt[2], v);
 }
 
 // Controller: every block updates its shared copy of the per-column state
@@ -370,7 +390,7 @@ struct BlockCounters {
 // Per-warp tile descriptors (rows of the tile, their masks and offsets).
 struct WarpTile {
     long long st[32];
-    int u[32], len[32], off[33];
+    int u[32], len[32], lenf[32], off[33], gtn[32];
     unsigned int em[32], chg[32];
 };
 
@@ -386,38 +406,203 @@ __device__ inline int tile_row_of(const int* off, int nrows, int g) {
     return lo;
 }
 
-// Round geometry, set with the round's actions (every CTA's controller):
-// the active columns (frontier | certify) and the step-major tile shape.
-// A warp tile holds rpt = 32 / na rows and lane (r, a) runs row r's ordered
-// sums for active column acol[a]; a window stages S consecutive entries of
-// EVERY row of the tile, so all lanes advance together (a certify round of
-// one column packs 32 rows per warp instead of idling 31 lanes).  Label
-// words are copied as one 8-byte word per entry when a single column is
-// active (span 1), else as the whole C-wide row.
-struct TileGeo {
-    int na, rpt, S, cmin, span;
-    int acol[kMaxCols];
-};
-constexpr int kMaxQ = DLP_WIN_MAX / 32;  // window slots per gathering lane
-// warp-private staging (doubles): DLP_WIN_MAX weights + kWin C-wide label rows
-__host__ __device__ inline int warp_smem_doubles(int C) { return DLP_WIN_MAX + (kWin * C > DLP_WIN_MAX ? kWin * C : DLP_WIN_MAX); }
+// ---------------------------------------------------------------------------
+// The LP view.  Within a batch the ground truth is fixed, so the parts of
+// _update_one (kernels/_csr.pyx:38-58) that only depend on it are constants
+// of the batch: w_all (every entry's weight, row order), w0 / w1 (weights of
+// class-0 / class-1 ground-truth neighbours, row order, per one-vs-rest
+// column) and the quotients w0 / w_all, w1 / w_all of the formula.  k_lp_view
+// computes them once per batch with the reference's summation order, and
+// writes each row's UNLABELED neighbours (row order kept) to a second pool at
+// the row's own offset.  The sweeps then only run the s chain
+// (s += (f[v] - fu) * w over unlabeled neighbours, the reference's order with
+// the ground-truth entries -- which add nothing to s -- left out): no
+// per-entry ground-truth test, no w_all / w0 / w1 chains, one division per
+// update instead of three.  Bit-identical: every value is produced by the
+// same IEEE operations on the same operands in the same order.
+// ---------------------------------------------------------------------------
+// vlen[u] carries the view length and, in bit 30, "the row has a ground-truth
+// neighbour": rows without one have w0 = w1 = 0, and their quotients are not
+// loaded (the formula's two products are then +-0.0, which leave fu + ...
+// unchanged exactly as the reference's (0 - fu) * (0 / w_all) terms do)
+constexpr int kVlenGt = 1 << 30;
+__device__ inline int vlen_len(int x) { return x & (kVlenGt - 1); }
 
-#ifndef DLP_LONG_RPT
-#define DLP_LONG_RPT 1  // rows per long-row tile (length imbalance wastes windows when > 1)
-#endif
+__global__ void k_lp_view(const int* elist, const DevState* ds, const long long* row_start, const int* row_len,
+                          const int* nbr, const double* wgt, const signed char* gt, int C, int* vnbr, double* vw,
+                          int* vlen, double* wsum, double* q01, const int* row_mod, int* view_b,
+                          long long* view_st, int seq, int inval) {
+    const int lane = threadIdx.x & 31;
+    const long long nw = (long long)gridDim.x * blockDim.x / 32;
+    const long long n = ds->n_elist;
+    const unsigned int below = (1u << lane) - 1u;
+    for (long long i = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / 32; i < n; i += nw) {
+        const int u = elist[i];
+        const long long st = row_start[u];
+        // cached: built after the row's last change, at its current offset,
+        // after the last repack of the pool
+        const int vb = view_b[u];
+        if (vb > 0 && vb >= row_mod[u] && vb > inval && view_st[u] == st) continue;
+        const int len = row_len[u];
+        double wa = 0.0, w0 = 0.0, w1 = 0.0;  // lane c < C: column c's w0 / w1
+        int cnt = 0;
+        for (int b = 0; b < len; b += 32) {
+            const int e = b + lane;
+            const bool valid = e < len;
+            const int y = valid ? nbr[st + e] : 0;
+            const double x = valid ? wgt[st + e] : 0.0;
+            const int g = valid ? (int)gt[y] : -1;
+            const bool unl = valid && g < 0;
+            const unsigned int m = __ballot_sync(0xffffffffu, unl);
+            if (unl) {
+                const long long p = st + cnt + __popc(m & below);
+                vnbr[p] = y;
+                vw[p] = x;
+            }
+            cnt += __popc(m);
+            const int nv = min(32, len - b);
+            for (int j = 0; j < nv; j++) wa = __dadd_rn(wa, __shfl_sync(0xffffffffu, x, j));
+            unsigned int gm = __ballot_sync(0xffffffffu, valid && g >= 0);
+            while (gm) {
+                const int j = __ffs(gm) - 1;
+                gm &= gm - 1;
+                const int gj = __shfl_sync(0xffffffffu, g, j);
+                const double xj = __shfl_sync(0xffffffffu, x, j);
+                if (lane < C) {
+                    const bool one = C == 1 ? gj == 1 : gj == lane;
+                    if (one)
+                        w1 = __dadd_rn(w1, xj);
+                    else
+                        w0 = __dadd_rn(w0, xj);
+                }
+            }
+        }
+        if (lane == 0) {
+            vlen[u] = cnt | (cnt < row_len[u] ? kVlenGt : 0);
+            wsum[u] = wa;
+            view_b[u] = seq;
+            view_st[u] = st;
+        }
+        if (lane < C) {
+            const long long q = ((long long)u * C + lane) * 2;
+            q01[q] = wa > 0.0 ? __ddiv_rn(w0, wa) : 0.0;
+            q01[q + 1] = wa > 0.0 ? __ddiv_rn(w1, wa) : 0.0;
+        }
+    }
+}
+
+// the label-difference sum of _update_one over a row's unlabeled neighbours
+struct RowS {
+    double s;
+    __device__ inline void init() { s = 0.0; }
+    template <int B>
+    __device__ inline void add_block(const double* w, const double* x, int xs, double fu) {
+        double p[B];
+#pragma unroll
+        for (int j = 0; j < B; j++) p[j] = __dmul_rn(__dsub_rn(x[j * xs], fu), w[j]);
+#pragma unroll
+        for (int j = 0; j < B; j++) s = __dadd_rn(s, p[j]);
+    }
+    __device__ inline void add(double w, double x, double fu) { s = __dadd_rn(s, __dmul_rn(__dsub_rn(x, fu), w)); }
+};
+
+// _csr.pyx:49-58 from the row constants: returns |fn - fu|, or -1 with value
+// 0.5 for the isolated sentinel (w_all <= 0)
+__device__ inline double finish_view(double s, double wall, const double* q, double fu, double* out) {
+    if (wall <= 0.0) {
+        *out = 0.5;
+        return -1.0;
+    }
+    const double a = __dmul_rn(__dsub_rn(0.0, fu), q[0]);
+    const double b = __dmul_rn(__dsub_rn(1.0, fu), q[1]);
+    const double c = __ddiv_rn(s, wall);
+    double fn = __dadd_rn(__dadd_rn(__dadd_rn(fu, a), b), c);
+    if (fn < 0.0)
+        fn = 0.0;
+    else if (fn > 1.0)
+        fn = 1.0;
+    *out = fn;
+    return fabs(__dsub_rn(fn, fu));
+}
+
+// Round geometry, set with the round's actions (every CTA's controller).
+// Two tile shapes:
+// * flat (many active columns): a tile holds rpt = 32 / C rows and lane
+//   (r, c) runs row r's sum for column c; a window stages the next kWin
+//   entries of the tile's concatenated rows, and a lane sums the part of its
+//   row inside the window.
+// * step-major (few active columns: na <= c_sm_max_na): rpt = 32 / na rows,
+//   lane (r, a) runs row r's sum for active column acol[a]; a window stages
+//   S consecutive entries of EVERY row of the tile so all lanes advance
+//   together (a certify round of one column packs 32 rows per warp instead of
+//   idling 31 lanes).  Label words are copied as one 8-byte word per entry
+//   when a single column is active (span 1), else as the whole C-wide row.  S
+//   is a multiple of the sum unroll U; slots past a row's end are staged as
+//   (w = 0, x = 0), which adds exactly nothing to s (s starts at +0.0 and is
+//   never -0.0), so the sums run in whole blocks of U.
+// The per-lane slot table and accumulate roles are computed once per round.
+constexpr int kQ = 2;  // window slots per gathering lane (step-major windows of <= 64 entries)
+constexpr int kWinW = 32 * kQ;
+// warp-private staging (doubles): kWinW weights, then the label words (at
+// least kWinW single words, or DLP_LABEL_WIN C-wide rows)
+constexpr int kRowConst = 96;  // per warp: (q0, q1) of each accumulate lane, w_all of each tile row
+__host__ __device__ inline int warp_smem_doubles(int C) {
+    return kWinW + (DLP_LABEL_WIN * C > kWinW ? DLP_LABEL_WIN * C : kWinW) + kRowConst;
+}
+// the row constants of the tile, copied asynchronously with the first
+// window's label words (sq = the warp's row-constant area)
+__device__ inline void tile_consts(const LPParams& P, const WarpTile& T, double* sq, int nrows, int ar, int ac,
+                                   bool aact, unsigned long long pol) {
+    const int lane = threadIdx.x & 31;
+    if (aact) {
+        if (T.gtn[ar]) {
+            cp_async16(sq + 2 * lane, P.q01 + ((long long)T.u[ar] * P.C + ac) * 2, pol);
+        } else {
+            sq[2 * lane] = 0.0;
+            sq[2 * lane + 1] = 0.0;
+        }
+    }
+    if (lane < nrows && T.em[lane]) cp_async8(sq + 64 + lane, P.wsum + T.u[lane], pol);
+}
+__constant__ int c_sm_max_na = DLP_SM_MAX_NA;
+struct TileGeo {
+    int flat, na, rpt, S, U, cmin, span;
+    int acol[kMaxCols];
+    unsigned char qr[kQ][32], qs[kQ][32];  // step-major: slot q of lane l -> tile row (32 = none), step
+    unsigned char ar[32], ac[32];          // accumulate role of lane l (ar = 32: none)
+};
+
 __device__ inline void set_geo(TileGeo& G, unsigned int act, int C, int xcap, int max_rows) {
     int na = 0;
     for (int c = 0; c < C; c++)
         if ((act >> c) & 1u) G.acol[na++] = c;
     if (na == 0) G.acol[na++] = 0;  // idle round (the loop is about to end)
+    G.flat = na > c_sm_max_na;
+    if (G.flat) {  // every column, identity roles
+        na = C;
+        for (int c = 0; c < C; c++) G.acol[c] = c;
+    }
     G.na = na;
     G.rpt = min(32 / na, max_rows);
     G.cmin = na == 1 ? G.acol[0] : 0;
     G.span = na == 1 ? 1 : C;
-    int we = xcap / G.span;  // label words fit in xcap doubles, weights in DLP_WIN_MAX
-    if (we > DLP_WIN_MAX) we = DLP_WIN_MAX;
-    int S = we / G.rpt;
-    G.S = S < 1 ? 1 : S;
+    int we = xcap / G.span;
+    if (we > kWinW) we = kWinW;
+    const int per = we / G.rpt;  // steps per row that fit
+    G.U = per >= 4 ? 4 : 2;
+    const int S = per / G.U * G.U;
+    G.S = S < G.U ? G.U : S;  // rpt * S <= kWinW always holds for U = 2
+    for (int l = 0; l < 32; l++) {
+        for (int q = 0; q < kQ; q++) {
+            const int j = l + 32 * q;
+            const int r = j / G.S;
+            G.qr[q][l] = (unsigned char)(r < G.rpt ? r : 32);
+            G.qs[q][l] = (unsigned char)(j - r * G.S);
+        }
+        const int r = l / na;
+        G.ar[l] = (unsigned char)(r < G.rpt ? r : 32);
+        G.ac[l] = (unsigned char)G.acol[l - r * na];
+    }
 }
 
 // Round context shared by the tile routine.
@@ -433,68 +618,37 @@ struct RoundCtx {
 // Row metadata of one tile row (lane r holds row r): loads issued one tile
 // ahead so their latency hides behind the current tile's gathers.
 struct TileMeta {
-    int u, len;
+    int u, len, lenf;  // view length (unlabeled neighbours, bit 30: ground-truth neighbour), full row length
     unsigned int em;
     long long st;
 };
 __device__ inline TileMeta load_meta(const LPParams& P, const RoundCtx& R, int u) {
-    TileMeta m{u, 0, 0u, 0};
+    TileMeta m{u, 0, 0, 0u, 0};
     if (u >= 0) {
         m.em = P.itlp ? (R.CE & P.eligm[u]) : (((R.fm_cur[u] & R.FR) | R.CE) & P.eligm[u]);
         m.st = P.row_start[u];
-        m.len = P.row_len[u];
+        m.len = P.vlen[u];
+        m.lenf = P.row_len[u];
     }
     return m;
 }
 
-// Per-lane constants of a round's geometry: the window slots this lane
-// gathers (slot j = lane + 32q -> tile row j / S, step j % S) and the
-// accumulate role (row ar, column ac).
-struct LaneGeo {
-    int qr[kMaxQ], qs[kMaxQ];
-    int ar, ac, acs;  // row, column, column offset inside the copied span
-    bool alane;       // lane has an accumulate role
-};
-__device__ inline LaneGeo lane_geo(const TileGeo& G, int lane) {
-    LaneGeo L;
-#pragma unroll
-    for (int q = 0; q < kMaxQ; q++) {
-        const int j = lane + 32 * q;
-        L.qr[q] = j < G.rpt * G.S ? j / G.S : 32;
-        L.qs[q] = j - (j / G.S) * G.S;
-    }
-    L.alane = lane < G.rpt * G.na;
-    L.ar = lane / G.na;
-    L.ac = G.acol[lane - L.ar * G.na];
-    L.acs = L.ac - G.cmin;
-    return L;
-}
-
-// Evaluate `nrows` consecutive work items W[k0 ..] as one step-major warp
-// tile (metadata m: lane r holds row r); `un` is the next tile's row of this
-// lane (-1 if none), whose metadata is loaded into *mn mid-tile.  Gathers are
-// entry-parallel into warp-private shared memory (ids and weights one window
-// ahead, label words by cp.async), then lane (row, column) runs the row's
-// sums in stored order (kernels/_csr.pyx:38-52); finally the changed rows
-// claim themselves and their neighbours (_csr.pyx:175-191).
-__device__ void warp_tile(const LPParams& P, const RoundCtx& R, const TileGeo& G, ClaimCtx& K,
-                          BlockCounters& B, WarpTile& T, double* sw, double* sx, long long k0, int nrows,
-                          unsigned long long pol, const TileMeta& m, int un, TileMeta* mn) {
-    const int C = P.C;
-    const LaneGeo L = lane_geo(G, threadIdx.x & 31);
+// Tile prologue shared by both shapes: publish the rows, count them.
+__device__ inline int tile_rows(const LPParams& P, const RoundCtx& R, BlockCounters& B, WarpTile& T, long long k0,
+                                int nrows, const TileMeta& m, int* maxlen_out) {
     const int lane = threadIdx.x & 31;
-    const int S = G.S, span = G.span;
-    // ---- tile rows
     int len = 0;
     unsigned int em = 0;
     if (lane < nrows) {
         em = m.em;
         P.emask_store[R.ybase + k0 + lane] = em;  // by work item: the commit reads it coalesced
-        len = em ? m.len : 0;
+        len = em ? vlen_len(m.len) : 0;
         T.u[lane] = m.u;
         T.em[lane] = em;
         T.st[lane] = em ? m.st : 0;
         T.len[lane] = len;
+        T.lenf[lane] = m.lenf;
+        T.gtn[lane] = (m.len & kVlenGt) != 0;
         T.chg[lane] = 0u;
     }
     int maxlen = len, total = len;
@@ -504,117 +658,59 @@ __device__ void warp_tile(const LPParams& P, const RoundCtx& R, const TileGeo& G
         total += __shfl_xor_sync(0xffffffffu, total, o);
     }
     if (R.tmax && len) atomicMax(R.tmax, (unsigned long long)len);
-    {
-        unsigned int nz = __ballot_sync(0xffffffffu, em != 0);
-        if (lane == 0 && nz) {
-            atomicAdd(&B.urows, (unsigned long long)__popc(nz));
-            atomicAdd(&B.uent, (unsigned long long)total);
-        }
+    const unsigned int nz = __ballot_sync(0xffffffffu, em != 0);
+    if (lane == 0 && nz) {
+        atomicAdd(&B.urows, (unsigned long long)__popc(nz));
+        atomicAdd(&B.uent, (unsigned long long)total);
     }
-    __syncwarp();  // T.* written by lane r is read by other lanes below
-    // accumulate role: lane (ar, ac); its own label fu is a plain load whose
-    // latency overlaps the first window's gathers
-    const bool aact = L.alane && L.ar < nrows && ((T.em[L.ar] >> L.ac) & 1u);
-    const int u_a = aact ? T.u[L.ar] : 0;
-    const int len_a = aact ? T.len[L.ar] : 0;
-    const double fu = aact ? ld_keep(P.X + (long long)u_a * C + L.ac, pol) : 0.0;
-    // gather role: slot q of this lane -> (row qr, step qs)
-    long long qst[kMaxQ];
-    int qlen[kMaxQ];
-#pragma unroll
-    for (int q = 0; q < kMaxQ; q++) {
-        const bool ok = L.qr[q] < nrows;
-        qst[q] = ok ? T.st[L.qr[q]] + L.qs[q] : 0;
-        qlen[q] = ok ? T.len[L.qr[q]] - L.qs[q] : 0;  // window wb is valid while wb < qlen
-    }
-    *mn = load_meta(P, R, un);  // next tile's metadata, consumed next iteration
-    RowAcc acc;
-    acc.init();
-    int vv[kMaxQ];
-    double ww[kMaxQ];
-    auto load_ids = [&](int wb) {
-#pragma unroll
-        for (int q = 0; q < kMaxQ; q++) {
-            if (wb < qlen[q]) {
-                vv[q] = __ldcs(P.nbr + qst[q] + wb);
-                ww[q] = __ldcs(P.w + qst[q] + wb);
-            }
-        }
-    };
-    if (maxlen > 0) load_ids(0);
-    const double* xcol = P.X + G.cmin;
-    for (int wb = 0; wb < maxlen; wb += S) {
-#pragma unroll
-        for (int q = 0; q < kMaxQ; q++) {
-            if (wb >= qlen[q]) continue;
-            const int j = lane + 32 * q;
-            sw[j] = ww[q];
-            if (span == 1)
-                cp_async8(sx + j, xcol + (long long)vv[q] * C, pol);
-            else
-                copy_label_row(sx + j * span, P.X + (long long)vv[q] * C, C, pol);
-        }
-        if (wb + S < maxlen) load_ids(wb + S);
-        cp_async_wait_all();
-        __syncwarp();
-        if (aact) {
-            const int hi = min(S, len_a - wb);
-            const double* w0p = sw + L.ar * S;
-            const double* x0p = sx + (L.ar * S) * span + L.acs;
-            int t = 0;
-            for (; t + kAccUnroll <= hi; t += kAccUnroll) acc.add_boxed_block<kAccUnroll>(w0p + t, x0p + t * span, span, fu);
-            for (; t < hi; t++) acc.add_boxed(w0p[t], x0p[t * span], fu);
-        }
-        __syncwarp();
-    }
-    // ---- finish: stage, count, flag
+    *maxlen_out = maxlen;
+    return total;
+}
+
+// Tile epilogue shared by both shapes: stage the new value of lane (ar, ac)'s
+// (row, column), count, and flag the columns that moved by more than delta.
+__device__ inline unsigned int tile_finish(const LPParams& P, const RoundCtx& R, ClaimCtx& K, const WarpTile& T,
+                                          const double* sq, long long k0, int ar, int ac, bool aact, double s,
+                                          double fu) {
     unsigned int ch = 0;
     if (aact) {
-        const int c = L.ac;
+        const int u = T.u[ar];
+        const int C = P.C;
         double val;
-        double d = acc.finish(fu, &val);
-        __stcs(P.Y + (R.ybase + k0 + L.ar) * C + c, val);
+        const double d = finish_view(s, sq[64 + ar], sq + 2 * (threadIdx.x & 31), fu, &val);
+        __stcs(P.Y + (R.ybase + k0 + ar) * C + ac, val);
         K.c_nev++;
-        K.c_edg += (unsigned long long)len_a;
+        K.c_edg += (unsigned long long)T.lenf[ar];
         if (d < 0.0) {  // isolated sentinel (_csr.pyx:49-51, 170-173)
             K.c_warn++;
-            atomicAnd(&P.eligm[u_a], ~(1u << c));
-            atomicAdd((unsigned long long*)&P.ctl->elig_count[c], ~0ULL);
+            atomicAnd(&P.eligm[u], ~(1u << ac));
+            atomicAdd((unsigned long long*)&P.ctl->elig_count[ac], ~0ULL);
         } else {
             K.c_rmax = fmax(K.c_rmax, d);
-            if (!P.itlp && d > P.delta) ch = 1u << c;
+            if (!P.itlp && d > P.delta) ch = 1u << ac;
         }
     }
-    if (P.itlp) return;
-    // ---- expand (jacobi_run commit loop, _csr.pyx:175-191)
-    if (!__any_sync(0xffffffffu, ch != 0)) return;
-    if (ch) atomicOr(&T.chg[L.ar], ch);
+    return ch;
+}
+
+// Expand (jacobi_run commit loop, _csr.pyx:175-191): the changed rows claim
+// themselves and their (unlabeled) neighbours -- ground-truth neighbours are
+// never eligible, so the view's entries are exactly the candidates.
+__device__ inline void tile_expand(const LPParams& P, const RoundCtx& R, ClaimCtx& K, WarpTile& T, long long k0,
+                                   int nrows, int ar, unsigned int ch) {
+    const int lane = threadIdx.x & 31;
+    if (ch) atomicOr(&T.chg[ar], ch);
     __syncwarp();
-    unsigned int mrow = lane < nrows ? T.chg[lane] : 0u;
+    const unsigned int mrow = lane < nrows ? T.chg[lane] : 0u;
     if (mrow) {
         K.claimed |= mrow;  // u changed, so u itself is eligible for those columns
         if (P.log_chg) P.log_chg[R.ybase + k0 + lane] = mrow;
         if (R.scan_mode)
-            atomicOr(&K.fm_next[T.u[lane]], mrow);
+            atomicOr(&K.fm_next()[T.u[lane]], mrow);
         else
             claim(K, T.u[lane], mrow);
     }
-    if (maxlen <= S) {
-        // single-window tile: the gathering lanes still hold the entries' ids
-#pragma unroll
-        for (int q = 0; q < kMaxQ; q++) {
-            if (qlen[q] <= 0) continue;
-            const unsigned int mq = T.chg[L.qr[q]];
-            if (!mq) continue;
-            if (R.scan_mode)
-                atomicOr(&K.fm_next[vv[q]], mq);  // no return value: a fire-and-forget RED
-            else
-                claim(K, vv[q], mq);
-        }
-        return;
-    }
-    // multi-window tile: walk the changed rows' entries, flattened
-    const int clen = mrow ? len : 0;
+    const int clen = mrow ? T.len[lane] : 0;
     int incl = clen;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -625,21 +721,205 @@ __device__ void warp_tile(const LPParams& P, const RoundCtx& R, const TileGeo& G
     const int ctot = __shfl_sync(0xffffffffu, incl, 31);
     __syncwarp();
     for (int g = lane; g < ctot; g += 32) {
-        int r = tile_row_of(T.off, nrows, g);
+        const int r = tile_row_of(T.off, nrows, g);
         const unsigned int mq = T.chg[r];
-        int v = __ldcs(P.nbr + T.st[r] + (g - T.off[r]));
+        const int v = __ldcs(P.vnbr + T.st[r] + (g - T.off[r]));
         if (R.scan_mode)
-            atomicOr(&K.fm_next[v], mq);
+            atomicOr(&K.fm_next()[v], mq);  // no return value: a fire-and-forget RED
         else
             claim(K, v, mq);
     }
+}
+
+// Flat tile: rows W[k0 ..] (metadata m, lane r holds row r); windows of kWin
+// entries of the concatenated rows, ids and weights loaded one window ahead,
+// label rows by cp.async; lane (r, c) sums its row's part of each window in
+// stored order.  `un` is the next tile's row of this lane (-1 if none),
+// whose metadata is loaded into *mn mid-tile.
+__device__ void warp_tile_flat(const LPParams& P, const RoundCtx& R, ClaimCtx& K, BlockCounters& B, WarpTile& T,
+                               double* sw, double* sx, double* sq, long long k0, int nrows, unsigned long long pol,
+                               const TileMeta& m, int un, TileMeta* mn) {
+    const int C = P.C;
+    const int lane = threadIdx.x & 31;
+    int maxlen;
+    const int total = tile_rows(P, R, B, T, k0, nrows, m, &maxlen);
+    int incl = lane < nrows ? T.len[lane] : 0;
+    __syncwarp();
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane < nrows) T.off[lane] = incl - T.len[lane];
+    __syncwarp();
+    const int ar = lane / C, ac = lane - ar * C;
+    const bool aact = ar < nrows && ((T.em[ar] >> ac) & 1u);
+    const double fu = aact ? ld_keep(P.X + (long long)T.u[ar] * C + ac, pol) : 0.0;
+    tile_consts(P, T, sq, nrows, ar, ac, aact, pol);
+    const int a_lo = aact ? T.off[ar] : 0, a_hi = aact ? T.off[ar] + T.len[ar] : 0;
+    *mn = load_meta(P, R, un);  // next tile's metadata, consumed next iteration
+    RowS acc;
+    acc.init();
+    int vv[kWin / 32], rr[kWin / 32];
+    double ww[kWin / 32];
+#pragma unroll
+    for (int j = 0; j < kWin / 32; j++) rr[j] = -1;  // a tile whose rows have no unlabeled entry runs no window
+    auto load_ids = [&](int wb) {
+        const int wn = min(kWin, total - wb);
+#pragma unroll
+        for (int j = 0; j < kWin / 32; j++) {
+            const int i = lane + 32 * j;
+            rr[j] = -1;
+            if (i < wn) {
+                const int g = wb + i;
+                const int r = tile_row_of(T.off, nrows, g);
+                const long long p = T.st[r] + (g - T.off[r]);
+                rr[j] = r;
+                vv[j] = __ldcs(P.vnbr + p);
+                ww[j] = __ldcs(P.vw + p);
+            }
+        }
+    };
+    if (total > 0) load_ids(0);
+    for (int wb = 0; wb < total; wb += kWin) {
+        const int wn = min(kWin, total - wb);
+#pragma unroll
+        for (int j = 0; j < kWin / 32; j++) {
+            if (rr[j] < 0) continue;
+            const int i = lane + 32 * j;
+            sw[i] = ww[j];
+            copy_label_row(sx + i * C, P.X + (long long)vv[j] * C, C, pol);
+        }
+        if (wb + kWin < total) load_ids(wb + kWin);
+        cp_async_wait_all();
+        __syncwarp();
+        if (aact) {
+            const int lo = max(a_lo, wb) - wb, hi = min(a_hi, wb + wn) - wb;
+            int t = lo;
+            for (; t + kAccUnroll <= hi; t += kAccUnroll) acc.add_block<kAccUnroll>(sw + t, sx + t * C + ac, C, fu);
+            for (; t < hi; t++) acc.add(sw[t], sx[t * C + ac], fu);
+        }
+        __syncwarp();
+    }
+    if (total == 0) {  // no window ran: the row constants' copies must still land
+        cp_async_wait_all();
+        __syncwarp();
+    }
+    const unsigned int ch = tile_finish(P, R, K, T, sq, k0, ar, ac, aact, acc.s, fu);
+    if (P.itlp) return;
+    if (!__any_sync(0xffffffffu, ch != 0)) return;
+    if (kExpandRegs && total <= kWin) {
+        // single-window tile: the gathering lanes still hold the entries' ids
+        if (ch) atomicOr(&T.chg[ar], ch);
+        __syncwarp();
+        const unsigned int mrow = lane < nrows ? T.chg[lane] : 0u;
+        if (mrow) {
+            K.claimed |= mrow;
+            if (P.log_chg) P.log_chg[R.ybase + k0 + lane] = mrow;
+            if (R.scan_mode)
+                atomicOr(&K.fm_next()[T.u[lane]], mrow);
+            else
+                claim(K, T.u[lane], mrow);
+        }
+#pragma unroll
+        for (int j = 0; j < kWin / 32; j++) {
+            if (rr[j] < 0) continue;
+            const unsigned int mq = T.chg[rr[j]];
+            if (!mq) continue;
+            if (R.scan_mode)
+                atomicOr(&K.fm_next()[vv[j]], mq);
+            else
+                claim(K, vv[j], mq);
+        }
+        return;
+    }
+    tile_expand(P, R, K, T, k0, nrows, ar, ch);
+}
+
+// Step-major tile (see TileGeo): S entries of every row per window, sums in
+// blocks of U over zero-padded row tails.
+template <int U>
+__device__ void warp_tile_sm(const LPParams& P, const RoundCtx& R, const TileGeo& G, ClaimCtx& K,
+                             BlockCounters& B, WarpTile& T, double* sw, double* sx, double* sq, long long k0,
+                             int nrows,
+                             unsigned long long pol, const TileMeta& m, int un, TileMeta* mn) {
+    const int C = P.C;
+    const int lane = threadIdx.x & 31;
+    const int S = G.S, span = G.span;
+    int maxlen;
+    tile_rows(P, R, B, T, k0, nrows, m, &maxlen);
+    __syncwarp();
+    const int ar = G.ar[lane], ac = G.ac[lane];
+    const bool aact = ar < nrows && ((T.em[ar] >> ac) & 1u);
+    const int len_a = aact ? T.len[ar] : 0;
+    const double fu = aact ? ld_keep(P.X + (long long)T.u[ar] * C + ac, pol) : 0.0;
+    tile_consts(P, T, sq, nrows, ar, ac, aact, pol);
+    *mn = load_meta(P, R, un);
+    RowS acc;
+    acc.init();
+    int vv[kQ];
+    double ww[kQ];
+    auto load_ids = [&](int wb) {
+#pragma unroll
+        for (int q = 0; q < kQ; q++) {
+            const int r = G.qr[q][lane];
+            if (r < nrows) {
+                const int e = wb + G.qs[q][lane];
+                if (e < T.len[r]) {
+                    const long long p = T.st[r] + e;
+                    vv[q] = __ldcs(P.vnbr + p);
+                    ww[q] = __ldcs(P.vw + p);
+                }
+            }
+        }
+    };
+    if (maxlen > 0) load_ids(0);
+    const double* xcol = P.X + G.cmin;
+    for (int wb = 0; wb < maxlen; wb += S) {
+#pragma unroll
+        for (int q = 0; q < kQ; q++) {
+            const int r = G.qr[q][lane];
+            if (r >= nrows) continue;
+            const int j = lane + 32 * q;
+            const int e = wb + G.qs[q][lane];
+            const int lr = T.len[r];
+            if (e < lr) {
+                sw[j] = ww[q];
+                if (span == 1)
+                    cp_async8(sx + j, xcol + (long long)vv[q] * C, pol);
+                else
+                    copy_label_row(sx + j * span, P.X + (long long)vv[q] * C, C, pol);
+            } else if (e - wb < ((lr - wb + U - 1) / U) * U) {  // pad the row's last block
+                sw[j] = 0.0;
+                for (int c = 0; c < span; c++) sx[j * span + c] = 0.0;
+            }
+        }
+        if (wb + S < maxlen) load_ids(wb + S);
+        cp_async_wait_all();
+        __syncwarp();
+        if (aact) {
+            const int hi = min(S, len_a - wb);
+            const double* w0p = sw + ar * S;
+            const double* x0p = sx + (ar * S) * span + (ac - G.cmin);
+            for (int t = 0; t < hi; t += U) acc.add_block<U>(w0p + t, x0p + t * span, span, fu);
+        }
+        __syncwarp();
+    }
+    if (maxlen == 0) {  // no window ran: the row constants' copies must still land
+        cp_async_wait_all();
+        __syncwarp();
+    }
+    const unsigned int ch = tile_finish(P, R, K, T, sq, k0, ar, ac, aact, acc.s, fu);
+    if (P.itlp) return;
+    if (!__any_sync(0xffffffffu, ch != 0)) return;
+    tile_expand(P, R, K, T, k0, nrows, ar, ch);
 }
 
 // Warp loop over the tiles of one row class: tile indices are grabbed two
 // ahead and row metadata one ahead (software pipeline), so a tile's
 // dependent chain of loads overlaps the previous tile's gathers.
 __device__ void warp_tiles(const LPParams& P, const RoundCtx& R, const TileGeo& G, ClaimCtx& K,
-                           BlockCounters& B, WarpTile& T, double* sw, double* sx, unsigned int* grab,
+                           BlockCounters& B, WarpTile& T, double* sw, double* sx, double* sq, unsigned int* grab,
                            long long nitems, unsigned long long pol) {
     const int lane = threadIdx.x & 31;
     const int per = G.rpt;
@@ -657,7 +937,12 @@ __device__ void warp_tiles(const LPParams& P, const RoundCtx& R, const TileGeo& 
         const int un = lane < nrn ? R.W[kn + lane] : -1;
         if (lane == 0 && kn < nitems) kr = atomicAdd(grab, (unsigned int)per);
         TileMeta mn;
-        warp_tile(P, R, G, K, B, T, sw, sx, k, nr, pol, m, un, &mn);
+        if (G.flat)
+            warp_tile_flat(P, R, K, B, T, sw, sx, sq, k, nr, pol, m, un, &mn);
+        else if (G.U == 4)
+            warp_tile_sm<4>(P, R, G, K, B, T, sw, sx, sq, k, nr, pol, m, un, &mn);
+        else
+            warp_tile_sm<2>(P, R, G, K, B, T, sw, sx, sq, k, nr, pol, m, un, &mn);
         __syncwarp();
         if (kn >= nitems) break;
         k = kn;
@@ -666,10 +951,12 @@ __device__ void warp_tiles(const LPParams& P, const RoundCtx& R, const TileGeo& 
     }
 }
 
-// Hub row (row_len > kHubRow) evaluated by the whole CTA: windows of
-// kHubWin entries are gathered by warps 1..7 (product terms precomputed)
-// into a double buffer while warp 0 (one lane per column) runs the ordered
-// sums over the previous window.
+// Hub row (view length > kHubRow) evaluated by the whole CTA, window by
+// window (kHubWin entries): warps 1-7 gather a window's ids, weights and
+// C-wide label rows and write the product terms (f[v] - fu) * w of every
+// column into a double buffer, while warp 0 (lane c = column c) runs the
+// s chain over the previous window's terms -- the only sequential part left
+// (w_all, w0, w1 are row constants of the view), one DADD per entry.
 __device__ void cta_hub_row(const LPParams& P, const RoundCtx& R, ClaimCtx& K, BlockCounters& B, double* buf,
                             double* s_fu, long long k, unsigned long long pol, int* s_i, long long* s_ll,
                             unsigned int* s_u32) {
@@ -683,7 +970,8 @@ __device__ void cta_hub_row(const LPParams& P, const RoundCtx& R, ClaimCtx& K, B
         s_i[0] = u;
         s_u32[0] = em;
         s_u32[1] = 0;
-        s_i[1] = em ? P.row_len[u] : 0;
+        s_i[1] = em ? vlen_len(P.vlen[u]) : 0;
+        s_i[3] = em ? P.row_len[u] : 0;
         s_ll[0] = em ? P.row_start[u] : 0;
         if (em) {
             if (R.tmax) atomicMax(R.tmax, (unsigned long long)s_i[1]);
@@ -694,21 +982,15 @@ __device__ void cta_hub_row(const LPParams& P, const RoundCtx& R, ClaimCtx& K, B
     __syncthreads();
     const unsigned int em = s_u32[0];
     if (!em) return;
-    const int u = s_i[0], len = s_i[1];
+    const int u = s_i[0], len = s_i[1], lenf = s_i[3];
     const long long st = s_ll[0];
-    if (tid < C) s_fu[tid] = ((em >> tid) & 1u) ? P.X[(long long)u * C + tid] : 0.0;
+    if (tid < C) s_fu[tid] = P.X[(long long)u * C + tid];
     __syncthreads();
     const int nwin = (len + kHubWin - 1) / kHubWin;
-    const int bsz = kHubWin * (C + 1);
-    // warps 0-3 run the row's four ordered sums (RowAcc::add_boxed split by
-    // accumulator: s, w_all, w0, w1; lane c = column c), so the sequential
-    // chains advance in parallel on four schedulers; warps 4-7 gather.  A
-    // gathering thread holds the ids and weights of its entries of the window
-    // after next in registers, so a window's gather is one round trip.
-    constexpr int kSumWarps = 4;
-    constexpr int kGth = kLpThreads - 32 * kSumWarps;
+    const int bsz = kHubWin * C;  // terms of one window
+    constexpr int kGth = kLpThreads - 32;
     constexpr int kPer = (kHubWin + kGth - 1) / kGth;
-    const int g = tid - 32 * kSumWarps;
+    const int g = tid - 32;
     int pv[kPer];
     double pw[kPer];
     auto load_ids = [&](int w) {
@@ -717,155 +999,75 @@ __device__ void cta_hub_row(const LPParams& P, const RoundCtx& R, ClaimCtx& K, B
         for (int j = 0; j < kPer; j++) {
             const int i = g + kGth * j;
             if (i < wn) {
-                pv[j] = __ldcs(P.nbr + st + wb + i);
-                pw[j] = __ldcs(P.w + st + wb + i);
+                pv[j] = __ldcs(P.vnbr + st + wb + i);
+                pw[j] = __ldcs(P.vw + st + wb + i);
             }
         }
     };
-    auto issue = [&](int w) {
-        double* sw = buf + (w & 1) * bsz;
-        double* sx = sw + kHubWin;
+    // terms of window w: label rows read straight into registers (16-byte
+    // loads when C is even), one product per column
+    auto terms = [&](int w) {
+        double* tb = buf + (w & 1) * bsz;
         const int wn = min(kHubWin, len - w * kHubWin);
 #pragma unroll
         for (int j = 0; j < kPer; j++) {
             const int i = g + kGth * j;
             if (i < wn) {
-                sw[i] = pw[j];
-                copy_label_row(sx + i * C, P.X + (long long)pv[j] * C, C, pol);
+                const double* xr = P.X + (long long)pv[j] * C;
+                if ((C & 1) == 0) {
+                    for (int c = 0; c < C; c += 2) {
+                        const double2 x2 = *(const double2*)(xr + c);
+                        tb[i * C + c] = __dmul_rn(__dsub_rn(x2.x, s_fu[c]), pw[j]);
+                        tb[i * C + c + 1] = __dmul_rn(__dsub_rn(x2.y, s_fu[c + 1]), pw[j]);
+                    }
+                } else {
+                    for (int c = 0; c < C; c++) tb[i * C + c] = __dmul_rn(__dsub_rn(ld_keep(xr + c, pol), s_fu[c]), pw[j]);
+                }
             }
         }
     };
-    if (warp >= kSumWarps) {
+    if (warp > 0) {
         load_ids(0);
-        issue(0);
+        terms(0);
         if (nwin > 1) load_ids(1);
-        cp_async_wait_all();
     }
     __syncthreads();
-    const bool act = warp < kSumWarps && lane < C && ((em >> lane) & 1u);
-    const double fu = act ? s_fu[lane] : 0.0;
-    double acc = 0.0;
-#ifdef DLP_HUBPROF
-    // diagnostics: cycles per part of the hub loop (warp 4 and warps 0-3, lane 0)
-    long long hp[3] = {0, 0, 0};
-#define HUBT(v) long long v = clock64()
-#else
-#define HUBT(v)
-#endif
+    const bool act = warp == 0 && lane < C && ((em >> lane) & 1u);
+    double s = 0.0;
     for (int w = 0; w < nwin; w++) {
-        HUBT(ta);
-        if (warp >= kSumWarps) {
+        if (warp > 0) {
             if (w + 1 < nwin) {
-                issue(w + 1);
+                terms(w + 1);
                 if (w + 2 < nwin) load_ids(w + 2);
-                HUBT(tb);
-                cp_async_wait_all();
-#ifdef DLP_HUBPROF
-                hp[0] += tb - ta;
-                hp[1] += clock64() - tb;
-#endif
             }
         } else if (act) {
-            // shared loads run a block of 8 entries ahead of the chain
-            const double* sw = buf + (w & 1) * bsz;
-            const double* sx = sw + kHubWin + lane;
+            const double* tb = buf + (w & 1) * bsz + lane;
             const int wn = min(kHubWin, len - w * kHubWin);
-            if (warp == 1) {  // w_all
-                int t = 0;
-                for (; t + 8 <= wn; t += 8) {
-                    double wv[8];
+            int t = 0;
+            for (; t + 8 <= wn; t += 8) {
+                double tv[8];
 #pragma unroll
-                    for (int j = 0; j < 8; j++) wv[j] = sw[t + j];
+                for (int j = 0; j < 8; j++) tv[j] = lds64(tb + (t + j) * C);
 #pragma unroll
-                    for (int j = 0; j < 8; j++) acc = __dadd_rn(acc, wv[j]);
-                }
-                for (; t < wn; t++) acc = __dadd_rn(acc, sw[t]);
-            } else if (warp == 0) {  // s: the label-difference sum
-                // terms of a block first (independent), then the chain
-                int t = 0;
-                for (; t + 8 <= wn; t += 8) {
-                    double tv[8], xv[8], wv[8];
-#pragma unroll
-                    for (int j = 0; j < 8; j++) {
-                        xv[j] = lds64(sx + (t + j) * C);
-                        wv[j] = lds64(sw + t + j);
-                    }
-#pragma unroll
-                    for (int j = 0; j < 8; j++) {
-                        const double p = __dmul_rn(__dsub_rn(xv[j], fu), wv[j]);
-                        tv[j] = is_boxed(xv[j]) ? 0.0 : p;
-                    }
-#pragma unroll
-                    for (int j = 0; j < 8; j++) acc = __dadd_rn(acc, tv[j]);
-                }
-                for (; t < wn; t++) {
-                    const double x = sx[t * C];
-                    acc = __dadd_rn(acc, is_boxed(x) ? 0.0 : __dmul_rn(__dsub_rn(x, fu), sw[t]));
-                }
-            } else {  // warp 2: w0, warp 3: w1 (weights of ground-truth neighbours per class)
-                const int cls_want = warp - 2;
-                int t = 0;
-                for (; t + 8 <= wn; t += 8) {
-                    double tv[8], xv[8], wv[8];
-#pragma unroll
-                    for (int j = 0; j < 8; j++) {
-                        xv[j] = lds64(sx + (t + j) * C);
-                        wv[j] = lds64(sw + t + j);
-                    }
-#pragma unroll
-                    for (int j = 0; j < 8; j++)
-                        tv[j] = (is_boxed(xv[j]) && boxed_class(xv[j]) == cls_want) ? wv[j] : 0.0;
-#pragma unroll
-                    for (int j = 0; j < 8; j++) acc = __dadd_rn(acc, tv[j]);
-                }
-                for (; t < wn; t++) {
-                    const double x = sx[t * C];
-                    acc = __dadd_rn(acc, (is_boxed(x) && boxed_class(x) == cls_want) ? sw[t] : 0.0);
-                }
+                for (int j = 0; j < 8; j++) s = __dadd_rn(s, tv[j]);
             }
-#ifdef DLP_HUBPROF
-            hp[0] += (long long)(__double_as_longlong(acc) & 0) + clock64() - ta;  // keep the chain before the stamp
-#endif
+            for (; t < wn; t++) s = __dadd_rn(s, tb[t * C]);
         }
-        HUBT(tc);
         __syncthreads();
-#ifdef DLP_HUBPROF
-        hp[2] += clock64() - tc;
-#endif
     }
-#ifdef DLP_HUBPROF
-    if (lane == 0 && P.ctl->prof) {
-        if (warp == kSumWarps) {
-            atomicAdd(&P.ctl->prof[0], (unsigned long long)hp[0]);
-            atomicAdd(&P.ctl->prof[1], (unsigned long long)hp[1]);
-            atomicAdd(&P.ctl->prof[2], (unsigned long long)hp[2]);
-        } else if (warp < kSumWarps) {
-            atomicAdd(&P.ctl->prof[3 + warp], (unsigned long long)hp[0]);
-            if (warp == 0) atomicAdd(&P.ctl->prof[7], (unsigned long long)hp[2]);
-        }
-    }
-#endif
-    double* chains = buf;  // [4][kMaxCols]: the windows are free now
-    if (act) chains[warp * kMaxCols + lane] = acc;
-    __syncthreads();
-    if (tid < C && ((em >> tid) & 1u)) {
-        RowAcc ra;
-        ra.s = chains[tid];
-        ra.w_all = chains[kMaxCols + tid];
-        ra.w0 = chains[2 * kMaxCols + tid];
-        ra.w1 = chains[3 * kMaxCols + tid];
+    if (act) {
         double val;
-        double d = ra.finish(s_fu[tid], &val);
-        __stcs(P.Y + (R.ybase + k) * C + tid, val);
-        atomicAdd(&B.neval[tid], 1ULL);
-        atomicAdd(&B.edges[tid], (unsigned long long)len);
+        const double d = finish_view(s, P.wsum[u], P.q01 + ((long long)u * C + lane) * 2, s_fu[lane], &val);
+        __stcs(P.Y + (R.ybase + k) * C + lane, val);
+        atomicAdd(&B.neval[lane], 1ULL);
+        atomicAdd(&B.edges[lane], (unsigned long long)lenf);
         if (d < 0.0) {
-            atomicAdd(&B.warn[tid], 1ULL);
-            atomicAnd(&P.eligm[u], ~(1u << tid));
-            atomicAdd((unsigned long long*)&P.ctl->elig_count[tid], ~0ULL);
+            atomicAdd(&B.warn[lane], 1ULL);
+            atomicAnd(&P.eligm[u], ~(1u << lane));
+            atomicAdd((unsigned long long*)&P.ctl->elig_count[lane], ~0ULL);
         } else {
-            if (d > 0.0) atomicMax(&B.rmax[tid], dbits(d));
-            if (!P.itlp && d > P.delta) atomicOr(&s_u32[1], 1u << tid);
+            if (d > 0.0) atomicMax(&B.rmax[lane], dbits(d));
+            if (!P.itlp && d > P.delta) atomicOr(&s_u32[1], 1u << lane);
         }
     }
     __syncthreads();
@@ -875,19 +1077,18 @@ __device__ void cta_hub_row(const LPParams& P, const RoundCtx& R, ClaimCtx& K, B
             K.claimed |= m;
             if (P.log_chg) P.log_chg[R.ybase + k] = m;
             if (R.scan_mode)
-                atomicOr(&K.fm_next[u], m);
+                atomicOr(&K.fm_next()[u], m);
             else
                 claim(K, u, m);
         }
         for (int t = tid; t < len; t += kLpThreads) {
-            int v = __ldcs(P.nbr + st + t);
+            int v = __ldcs(P.vnbr + st + t);
             if (R.scan_mode)
-                atomicOr(&K.fm_next[v], m);
+                atomicOr(&K.fm_next()[v], m);
             else
                 claim(K, v, m);
         }
     }
-    (void)lane;
     __syncthreads();
 }
 
@@ -899,6 +1100,7 @@ __global__ void __launch_bounds__(kLpThreads, DLP_LP_MINB) k_lp_fused(LPParams P
     extern __shared__ double smem_dyn[];
     __shared__ ColState S;
     __shared__ TileGeo s_geo, s_geo_l;  // short-row / long-row tile shapes
+    __shared__ ClaimTargets s_ct;        // the round's claim targets
     __shared__ BlockCounters B;
     __shared__ WarpTile TT[kLpThreads / 32];
     __shared__ unsigned long long s_res[4 * kMaxCols];
@@ -917,7 +1119,8 @@ __global__ void __launch_bounds__(kLpThreads, DLP_LP_MINB) k_lp_fused(LPParams P
     unsigned int target = 0;
     const int wsm = warp_smem_doubles(C);  // warp-private staging: weights, then label words
     double* sw = smem_dyn + warp * wsm;
-    double* sx = sw + DLP_WIN_MAX;
+    double* sx = sw + kWinW;
+    double* sq = sw + wsm - kRowConst;  // row constants of the current tile
     WarpTile& T = TT[warp];
     const unsigned int allc = C >= 32 ? 0xffffffffu : ((1u << C) - 1u);
     const unsigned long long pol = l2_evict_last_policy();
@@ -935,7 +1138,7 @@ __global__ void __launch_bounds__(kLpThreads, DLP_LP_MINB) k_lp_fused(LPParams P
             P.fmask[0][u] = allc;
             // one call site per class: append_u32 aggregates over the converged
             // threads, which must all target the same list
-            switch (row_class(P.row_len[u])) {
+            switch (row_class(vlen_len(P.vlen[u]))) {
                 case CLS_SHORT: append_u32(P.flist[0][0], &ctl->n_f0[0], u); break;
                 case CLS_LONG: append_u32(P.flist[1][0], &ctl->n_f0[1], u); break;
                 default: append_u32(P.flist[2][0], &ctl->n_f0[2], u); break;
@@ -943,7 +1146,7 @@ __global__ void __launch_bounds__(kLpThreads, DLP_LP_MINB) k_lp_fused(LPParams P
         }
         for (long long i = gtid; i < n_el; i += gth) {
             int u = P.elist[i];
-            const int cls = row_class(P.row_len[u]);
+            const int cls = row_class(vlen_len(P.vlen[u]));
             P.eligm[u] |= (unsigned int)cls << kClassShift;
             switch (cls) {
                 case CLS_SHORT: append_u32(P.elist_c[0], &ctl->n_el[0], u); break;
@@ -975,8 +1178,8 @@ __global__ void __launch_bounds__(kLpThreads, DLP_LP_MINB) k_lp_fused(LPParams P
             decide_actions_act(S, P, nullptr, nullptr, 1);
         else
             decide_actions(S, P, nullptr, nullptr, 1);
-        set_geo(s_geo, S.fr_mask | S.cert_mask, C, wsm - DLP_WIN_MAX, 32);
-        set_geo(s_geo_l, S.fr_mask | S.cert_mask, C, wsm - DLP_WIN_MAX, DLP_LONG_RPT);
+        set_geo(s_geo, S.fr_mask | S.cert_mask, C, wsm - kWinW - kRowConst, 32);
+        set_geo(s_geo_l, S.fr_mask | S.cert_mask, C, wsm - kWinW - kRowConst, DLP_LONG_RPT);
     }
     long long nel[3], ncur[3];
     for (int j = 0; j < 3; j++) {
@@ -1002,8 +1205,8 @@ __global__ void __launch_bounds__(kLpThreads, DLP_LP_MINB) k_lp_fused(LPParams P
         const bool scan_mode = !P.itlp && nwork * kScanRatio >= n;
         unsigned int* fm_cur = P.fmask[ri];
         unsigned int* fm_next = P.fmask[rn];
-        ClaimCtx K{fm_next, {P.flist[0][rn], P.flist[1][rn], P.flist[2][rn]}, slot->cnt, P.eligm, P.row_len, 0u,
-                   0ULL, 0ULL, 0u, 0.0};
+        if (tid == 0) s_ct = ClaimTargets{fm_next, {P.flist[0][rn], P.flist[1][rn], P.flist[2][rn]}, slot->cnt, P.eligm};
+        ClaimCtx K{&s_ct, 0u, 0u, 0u, 0ULL, 0.0};
         if (tid < kMaxCols) {
             B.rmax[tid] = 0;
             B.neval[tid] = 0;
@@ -1044,9 +1247,9 @@ __global__ void __launch_bounds__(kLpThreads, DLP_LP_MINB) k_lp_fused(LPParams P
             RoundCtx RL{W1, n0c, FR, CE, fm_cur, scan_mode, tmax};
             RoundCtx RS{W0, 0, FR, CE, fm_cur, scan_mode, tmax};
             if (prof) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tw1));
-            warp_tiles(P, RL, s_geo_l, K, B, T, sw, sx, &slot->grab[1], n1c, pol);  // long rows
+            warp_tiles(P, RL, s_geo_l, K, B, T, sw, sx, sq, &slot->grab[1], n1c, pol);  // long rows
             if (prof) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tw2));
-            warp_tiles(P, RS, s_geo, K, B, T, sw, sx, &slot->grab[0], n0c, pol);  // short rows
+            warp_tiles(P, RS, s_geo, K, B, T, sw, sx, sq, &slot->grab[0], n0c, pol);  // short rows
             if (prof) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tw3));
             if (prof) {  // warp-time per part of phase 1 (diagnostics)
                 atomicAdd(&ctl->prof[0], tw1 - tw0);
@@ -1056,8 +1259,8 @@ __global__ void __launch_bounds__(kLpThreads, DLP_LP_MINB) k_lp_fused(LPParams P
         }
         if (K.claimed) atomicOr(&B.claimed, K.claimed);
         if (K.c_nev) {  // lane (row, a) of every tile of the round works on column acol[a]
-            const int col = s_geo.acol[lane % s_geo.na];
-            atomicAdd(&B.neval[col], K.c_nev);
+            const int col = s_geo.ac[lane];
+            atomicAdd(&B.neval[col], (unsigned long long)K.c_nev);
             atomicAdd(&B.edges[col], K.c_edg);
             if (K.c_warn) atomicAdd(&B.warn[col], (unsigned long long)K.c_warn);
             if (K.c_rmax > 0.0) atomicMax(&B.rmax[col], dbits(K.c_rmax));
@@ -1219,8 +1422,8 @@ __global__ void __launch_bounds__(kLpThreads, DLP_LP_MINB) k_lp_fused(LPParams P
                     decide_actions_act(S, P, s_res, &s_claimed, 0);
                 else
                     decide_actions(S, P, s_res, &s_claimed, 0);
-                set_geo(s_geo, S.fr_mask | S.cert_mask, C, wsm - DLP_WIN_MAX, 32);
-                set_geo(s_geo_l, S.fr_mask | S.cert_mask, C, wsm - DLP_WIN_MAX, DLP_LONG_RPT);
+                set_geo(s_geo, S.fr_mask | S.cert_mask, C, wsm - kWinW - kRowConst, 32);
+                set_geo(s_geo_l, S.fr_mask | S.cert_mask, C, wsm - kWinW - kRowConst, DLP_LONG_RPT);
             }
         }
         for (int j = 0; j < 3; j++) ncur[j] = s_cnt[j];
@@ -1316,7 +1519,11 @@ void lp_setup(Engine& E) {
     l2_setup(E);
     if (E.ncol > kMaxCols) throw CudaFailure(cudaErrorInvalidValue, "ncol > kMaxCols", __FILE__, __LINE__);
     E.lp_smem = std::max((size_t)(kLpThreads / 32) * warp_smem_doubles(E.ncol),
-                         (size_t)2 * kHubWin * (E.ncol + 1)) * sizeof(double);
+                         (size_t)2 * kHubWin * E.ncol) * sizeof(double);
+    if (const char* v = getenv("DLP_SM_MAX_NA")) {
+        int x = atoi(v);
+        DLP_CUDA_TRY(cudaMemcpyToSymbol(c_sm_max_na, &x, sizeof(int)));
+    }
     DLP_CUDA_TRY(cudaFuncSetAttribute(k_lp_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)E.lp_smem));
     if (const char* v = getenv("DLP_CARVEOUT"))  // shared-memory share of L1 (percent), tuning
         DLP_CUDA_TRY(cudaFuncSetAttribute(k_lp_fused, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(v)));
@@ -1339,9 +1546,39 @@ void lp_setup(Engine& E) {
     for (auto& ev : E.lp_ev) DLP_CUDA_TRY(cudaEventCreate(&ev));
 }
 
+// The batch's LP view (k_lp_view) over the eligible list; the view pool is
+// the adjacency pool's compaction target (free between structure updates).
+// Rows unchanged since their view was built keep it (row_mod from the
+// batch's affected marks, view_b / view_st of the build, view_inval after a
+// pool repack), so a batch rebuilds only the rows it touched.
+void lp_build_view(Engine& E) {
+    cudaStream_t st = E.st;
+    if (E.nbr_sp.n < E.nbr.n || E.wgt_sp.n < E.wgt.n) {
+        E.nbr_sp.reserve(E.nbr.n, 0, st);
+        E.wgt_sp.reserve(E.wgt.n, 0, st);
+        E.view_inval = E.view_seq - 1;
+    }
+    k_lp_view<<<E.sm_count * 8, kLpThreads, 0, st>>>(E.elist.p, E.ds, E.row_start.p, E.row_len.p, E.nbr.p, E.wgt.p,
+                                                     E.gt.p, E.ncol, E.nbr_sp.p, E.wgt_sp.p, E.vlen.p, E.wsum.p,
+                                                     E.q01.p, E.row_mod.p, E.view_b.p, E.view_st.p, E.view_seq,
+                                                     E.view_inval);
+    DLP_CUDA_TRY(cudaGetLastError());
+    E.launches++;
+}
+
+static void view_params(Engine& E, LPParams& P) {
+    P.vnbr = E.nbr_sp.p;
+    P.vw = E.wgt_sp.p;
+    P.vlen = E.vlen.p;
+    P.wsum = E.wsum.p;
+    P.q01 = E.q01.p;
+}
+
 void lp_run_dev(Engine& E, double delta, long long max_iter, bool itlp) {
     lp_setup(E);
+    lp_build_view(E);
     LPParams P;
+    view_params(E, P);
     P.row_start = E.row_start.p;
     P.row_len = E.row_len.p;
     P.nbr = E.nbr.p;
@@ -1404,7 +1641,9 @@ void lp_run_dev(Engine& E, double delta, long long max_iter, bool itlp) {
 // ctl->act / ctl->budget; first = first launch of the batch (full reset).
 void lp_run_actions(Engine& E, double delta, bool first, bool cleanup) {
     lp_setup(E);
+    if (first && !cleanup) lp_build_view(E);
     LPParams P;
+    view_params(E, P);
     P.row_start = E.row_start.p;
     P.row_len = E.row_len.p;
     P.nbr = E.nbr.p;
@@ -1471,7 +1710,11 @@ void lp_run_actions(Engine& E, double delta, bool first, bool cleanup) {
 // One warp per remote row.
 __global__ void k_rows_apply(long long m, int C, const int* ru, const unsigned int* rem, const unsigned int* rchg,
                              const double* rval, double* X, const long long* row_start, const int* row_len,
-                             const int* nbr, ClaimCtx K, int* has_fr) {
+                             const int* nbr, ClaimTargets tg, int* has_fr) {
+    __shared__ ClaimTargets s_tg;
+    if (threadIdx.x == 0) s_tg = tg;
+    __syncthreads();
+    ClaimCtx K{&s_tg, 0u, 0u, 0u, 0ULL, 0.0};
     const int lane = threadIdx.x & 31;
     const long long wid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
     const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
@@ -1493,13 +1736,76 @@ __global__ void k_rows_apply(long long m, int C, const int* ru, const unsigned i
 void lp_rows_apply(Engine& E, long long m, long long r_par) {
     if (m <= 0) return;
     const int ri = (int)(r_par & 1);
-    ClaimCtx K{E.fmask[ri].p, {E.ulist[ri].p, E.llist[ri].p, E.hlist[ri].p}, E.ctl->ncur_p, E.eligm.p, E.row_len.p,
-               0u, 0ULL, 0ULL, 0u, 0.0};
+    ClaimTargets K{E.fmask[ri].p, {E.ulist[ri].p, E.llist[ri].p, E.hlist[ri].p}, E.ctl->ncur_p, E.eligm.p};
     const long long blocks = std::min<long long>((m * 32 + kBlock - 1) / kBlock, (long long)E.sm_count * 16);
     k_rows_apply<<<(unsigned int)blocks, kBlock, 0, E.st>>>(m, E.ncol, E.rx_u.p, E.rx_em.p, E.rx_chg.p, E.rx_val.p,
                                                            E.f[0].p, E.row_start.p, E.row_len.p, E.nbr.p, K,
                                                            E.ctl->has_fr);
     DLP_CUDA_TRY(cudaGetLastError());
+    E.launches++;
+}
+
+// Row partition over NCCL: pack the round's evaluated rows (record = vertex,
+// evaluated mask, changed mask, C label words) into the send buffer; the
+// changed-mask log is cleared for the next round as it is read.
+__global__ void k_rows_pack(long long n, int C, const int* lu, const unsigned int* lem, unsigned int* lchg,
+                            const double* Y, unsigned long long* send, unsigned long long* count) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const unsigned int em = lem[i];
+        const unsigned int chg = lchg[i];
+        lchg[i] = 0u;
+        if (!em) continue;
+        const unsigned long long j = atomicAdd(count, 1ULL);
+        unsigned long long* r = send + j * (3 + C);
+        r[0] = (unsigned long long)lu[i];
+        r[1] = em;
+        r[2] = chg;
+        for (int c = 0; c < C; c++) r[3 + c] = (unsigned long long)__double_as_longlong(Y[i * C + c]);
+    }
+}
+
+void rows_pack(Engine& E, long long n, unsigned long long* send, unsigned long long* count) {
+    if (n <= 0) return;
+    k_rows_pack<<<blocks_for(n), kBlock, 0, E.st>>>(n, E.ncol, E.log_u.p, E.log_em.p, E.log_chg.p, E.f[1].p, send,
+                                                    count);
+    DLP_CUDA_TRY(cudaGetLastError());
+    E.launches++;
+}
+
+// the other ranks' records -> k_rows_apply inputs (rank r's record j goes to
+// base[r] + j; meta = [cnt[0..W), base[0..W)])
+__global__ void k_rows_unpack(int W, int me, long long mx, int C, const long long* meta,
+                              const unsigned long long* recv, int* ru, unsigned int* rem, unsigned int* rchg,
+                              double* rval) {
+    const long long tot = (long long)W * mx;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < tot; t += (long long)gridDim.x * blockDim.x) {
+        const int r = (int)(t / mx);
+        const long long j = t - r * mx;
+        if (r == me || j >= meta[r]) continue;
+        const long long o = meta[W + r] + j;
+        const unsigned long long* rec = recv + t * (3 + C);
+        ru[o] = (int)rec[0];
+        rem[o] = (unsigned int)rec[1];
+        rchg[o] = (unsigned int)rec[2];
+        for (int c = 0; c < C; c++) rval[o * C + c] = __longlong_as_double((long long)rec[3 + c]);
+    }
+}
+
+void rows_unpack(Engine& E, int W, int me, long long mx, const std::vector<unsigned long long>& cnt,
+                 const std::vector<long long>& base, const unsigned long long* recv) {
+    std::vector<long long> meta(2 * W);
+    for (int r = 0; r < W; r++) {
+        meta[r] = (long long)cnt[r];
+        meta[W + r] = base[r];
+    }
+    E.comm_buf.reserve(2 * (size_t)W + 2 + 2 * (size_t)W, 2 * (size_t)W + 2, E.st);
+    long long* md = (long long*)(E.comm_buf.p + 2 * W + 2);
+    DLP_CUDA_TRY(cudaMemcpyAsync(md, meta.data(), meta.size() * 8, cudaMemcpyHostToDevice, E.st));
+    const long long tot = (long long)W * mx;
+    k_rows_unpack<<<blocks_for(tot), kBlock, 0, E.st>>>(W, me, mx, E.ncol, md, recv, E.rx_u.p, E.rx_em.p,
+                                                        E.rx_chg.p, E.rx_val.p);
+    DLP_CUDA_TRY(cudaGetLastError());
+    DLP_CUDA_TRY(cudaStreamSynchronize(E.st));  // meta is a host temporary
     E.launches++;
 }
 
@@ -1528,11 +1834,13 @@ void lp_dump_trace(Engine& E, long long rounds) {
 // isolated unlabeled vertices are pinned to 0.5 and counted.
 // ---------------------------------------------------------------------------
 __global__ void k_itlp_active(long long n, const unsigned char* alive, const signed char* gt, const int* row_len,
-                              int ncol, double* f0, double* f1, unsigned int* eligm, int* alist, DevState* ds) {
+                              int ncol, double* f0, double* f1, unsigned int* eligm, int* alist, DevState* ds,
+                              const unsigned char* mark, int* row_mod, int seq) {
     unsigned int allc = ncol >= 32 ? 0xffffffffu : ((1u << ncol) - 1u);
     long long iso = 0;
     for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < n; v += (long long)gridDim.x * blockDim.x) {
         bool unl = alive[v] && gt[v] == -1;
+        if (mark[v]) row_mod[v] = seq;
         eligm[v] = (unl && row_len[v] > 0) ? allc : 0u;
         if (!unl) continue;
         if (row_len[v] > 0) {
@@ -1553,7 +1861,7 @@ void itlp_active_dev(Engine& E, long long n) {
     if (n == 0) return;
     k_itlp_active<<<blocks_for(n, kBlock, 148 * 64), kBlock, 0, E.st>>>(n, E.alive.p, E.gt.p, E.row_len.p, E.ncol,
                                                                        E.f[0].p, E.f[1].p, E.eligm.p, E.elist.p,
-                                                                       E.ds);
+                                                                       E.ds, E.mark.p, E.row_mod.p, E.view_seq);
     E.launches++;
 }
 

@@ -82,10 +82,15 @@ class InProcessCollective:
 class ShardedGraph(DynamicGraph):
     """DynamicGraph holding this rank's share of the propagation."""
 
-    MODES = {"components": 0, "rows": 1}
+    # components: sticky LPT placement by edge count; components_hash: placement by
+    # a hash of the component root; rows: row partition for one giant component
+    MODES = {"components": 0, "rows": 1, "components_hash": 2}
 
-    def __init__(self, device: int, num_classes: int, rank: int, world: int, collective: Collective,
-                 mode: str = "components") -> None:
+    def __init__(self, device: int, num_classes: int, rank: int, world: int, collective: Optional[Collective],
+                 mode: str = "components", nccl_id: Optional[bytes] = None) -> None:
+        """collective: a host reduction (torch.distributed, in-process for
+        virtual shards); or None with nccl_id: the engine's own NCCL
+        communicator, every exchange on device buffers (dlp_shard_nccl)."""
         super().__init__(device, num_classes)
         if mode not in self.MODES:
             raise ValueError(f"unknown shard mode {mode!r}")
@@ -93,6 +98,13 @@ class ShardedGraph(DynamicGraph):
         self._check(self._lib.dlp_shard_set(self._h, self.rank, self.world))
         self._check(self._lib.dlp_shard_mode(self._h, self.MODES[mode]))
         self._collective = collective
+        self._cb = None
+        if collective is None:
+            if nccl_id is None or len(nccl_id) != 128:
+                raise ValueError("a collective or a 128-byte NCCL id is required")
+            buf = C.create_string_buffer(bytes(nccl_id), 128)
+            self._check(self._lib.dlp_shard_nccl(self._h, buf, self.world, self.rank))
+            return
 
         def cb(ctx, imax, nimax, isum, nisum, dmax, ndmax):
             try:
@@ -118,11 +130,32 @@ class ShardedGraph(DynamicGraph):
                           _native.ptr(other), _native.ptr(w), len(dels), _native.ptr(dels))
         reps = (_native.Report * self.ncol)()
         c = cfg._c(self.num_classes)
-        rc = self._lib.dlp_apply_batch_sharded(self._h, C.byref(c), C.byref(b), C.cast(self._cb, C.c_void_p), None,
-                                                reps)
+        cb = C.cast(self._cb, C.c_void_p) if self._cb is not None else None  # None: the engine's NCCL
+        rc = self._lib.dlp_apply_batch_sharded(self._h, C.byref(c), C.byref(b), cb, None, reps)
         self._version += 1
         self._check(rc)
         return _reports(reps, "dynlp")
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh NCCL unique id (rank 0 makes it, the caller broadcasts it)."""
+    lib = _native.load()
+    buf = C.create_string_buffer(128)
+    rc = lib.dlp_nccl_unique_id(buf)
+    if rc != 0:
+        raise RuntimeError("ncclGetUniqueId failed (libnccl.so.2 missing?)")
+    return buf.raw
+
+
+def nccl_sharded_graph(device: int, num_classes: int, mode: str = "components", group=None) -> "ShardedGraph":
+    """A ShardedGraph for this torch.distributed rank whose exchanges run on
+    the engine's own NCCL communicator (the id travels over `group`)."""
+    import torch.distributed as dist
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    obj = [nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    return ShardedGraph(device, num_classes, rank, world, None, mode, nccl_id=obj[0])
 
 
 def apply_batch_sharded(graph: ShardedGraph, labels: LabelState, batch, cfg: EngineConfig):

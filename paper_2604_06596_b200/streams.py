@@ -131,6 +131,32 @@ def knn_graph_torch64(x: np.ndarray, k: int, device: str = "cuda", block: int = 
     return _symmetrize(np.concatenate(srcs), np.concatenate(dsts), np.concatenate(sims), n)
 
 
+def uniform_cube(n: int, seed: int) -> Blobs:
+    """n points uniform in [0, 1]^3, class = x > 1/2 (SURVEY.md §8(d) D-2 C5:
+    a single giant component with high probability at k = 10)."""
+    rng = np.random.default_rng(seed)
+    x = rng.random((n, 3))
+    return Blobs(x, (x[:, 0] > 0.5).astype(np.int8))
+
+
+def knn_graph_grid3d(x: np.ndarray, k: int, workers: int = -1) -> EdgeList:
+    """Exact Euclidean k-NN of 3-D points (a k-d tree, the low-dimensional
+    analogue of the grid search; ties to the lower id by stable id order),
+    union-symmetrised with max-merge like builder.py:77-92.  Weight
+    exp(-d^2 / 2h^2), h = the expected k-NN radius of a uniform cloud, so
+    weights lie in (0, 1]."""
+    from scipy.spatial import cKDTree
+
+    n = x.shape[0]
+    tree = cKDTree(x, leafsize=32, balanced_tree=False, compact_nodes=False)
+    dist, idx = tree.query(x, k=k + 1, workers=workers)
+    dist, idx = dist[:, 1:], idx[:, 1:]  # drop self
+    h = (k / (n * 4.0 / 3.0 * np.pi)) ** (1.0 / 3.0)
+    sim = np.exp(-(dist * dist) / (2.0 * h * h)).reshape(-1)
+    src = np.repeat(np.arange(n, dtype=np.int64), k)
+    return _symmetrize(src, idx.reshape(-1).astype(np.int64), sim, n)
+
+
 def erdos_renyi_edges(n: int, avg_degree: float, seed: int, low=0.1, high=1.0) -> EdgeList:
     rng = np.random.default_rng(seed)
     m = int(rng.binomial(n * (n - 1) // 2, min(1.0, avg_degree / max(1, n - 1))))

@@ -156,7 +156,7 @@ def _stream(kind):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("kind,world,mode", [("blobs2", 2, "components"), ("blobs10", 2, "components"),
-                                             ("blobs10", 3, "components"), ("blobs2", 2, "rows"),
+                                             ("blobs10", 3, "components"), ("blobs10", 3, "components_hash"), ("blobs2", 2, "rows"),
                                              ("blobs10", 3, "rows"), ("giant", 2, "rows"), ("giant", 4, "rows")])
 def test_virtual_shards_bit_identical(gpu_device, kind, world, mode):
     from paper_2604_06596_b200.engine import EngineConfig
@@ -175,3 +175,56 @@ def test_virtual_shards_bit_identical(gpu_device, kind, world, mode):
                   b.certify_sweeps)
             assert ta == tb, f"batch {t} column {c}: {ta} != {tb}"
         assert Fw.tobytes() == Fg.tobytes(), f"batch {t}: labels differ"
+
+
+def _nccl_id_worker(rank, world, port, q):
+    sys.path.insert(0, os.path.dirname(HERE))
+    import torch.distributed as dist
+
+    from paper_2604_06596_b200.sharded import nccl_unique_id
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    obj = [nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    q.put((rank, obj[0]))
+    dist.destroy_process_group()
+
+
+def test_nccl_id_broadcast_gloo_world2():
+    """The host plumbing of the in-handle NCCL communicator: rank 0's 128-byte
+    ncclUniqueId (libnccl via the engine library) reaches every rank intact."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_nccl_id_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    got = dict(q.get(timeout=120) for _ in range(2))
+    for p in ps:
+        p.join(timeout=60)
+    assert len(got[0]) == 128 and got[0] == got[1]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind,mode", [("blobs10", "components"), ("giant", "rows")])
+def test_nccl_in_handle_world1(gpu_device, kind, mode):
+    """The engine's own NCCL communicator (world 1 on the one GPU): every
+    exchange -- phase all-reduces, migration, the row all-gather of packed
+    device records -- runs as an NCCL collective; bit-identical to the
+    unsharded engine."""
+    from paper_2604_06596_b200.engine import EngineConfig, LabelState
+    from paper_2604_06596_b200.sharded import ShardedGraph, apply_batch_sharded, nccl_unique_id
+
+    batches, ncls = _stream(kind)
+    cfg = EngineConfig(delta=1e-5)
+    want = _unsharded(batches, cfg, ncls)
+    g = ShardedGraph(0, ncls, 0, 1, None, mode, nccl_id=nccl_unique_id())
+    lab = LabelState()
+    for t, (b, (rw, Fw)) in enumerate(zip(batches, want)):
+        lab, rg = apply_batch_sharded(g, lab, b, cfg)
+        rg = rg if isinstance(rg, list) else [rg]
+        for c, (a, x) in enumerate(zip(rw, rg)):
+            assert (a.iterations, a.updates, a.max_change, a.converged, a.warnings) == \
+                (x.iterations, x.updates, x.max_change, x.converged, x.warnings), (t, c)
+        assert lab.F.tobytes() == Fw.tobytes(), f"batch {t}: labels differ"
+    g.close()
