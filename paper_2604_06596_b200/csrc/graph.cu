@@ -1198,7 +1198,8 @@ __global__ void k_migr_unpack(const int* list, long long m, int ncol, const doub
 
 long long migr_collect(Engine& E, long long n) {
     cudaStream_t st = E.st;
-    if (n == 0) return 0;
+    // migration flags exist only for component sharding over several ranks
+    if (n == 0 || E.shard_world <= 1 || E.shard_rows) return 0;
     cub_scan(E, E.migr_flag.p, E.migr_pos.p, n);
     int lp = 0, lf = 0;
     DLP_CUDA_TRY(cudaMemcpyAsync(&lp, E.migr_pos.p + n - 1, sizeof(int), cudaMemcpyDeviceToHost, st));

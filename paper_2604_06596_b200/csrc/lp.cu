@@ -54,16 +54,10 @@ namespace dlp {
 
 constexpr int kLpThreads = 256;
 #ifndef DLP_WIN
-#define DLP_WIN 32
-#endif
-#ifndef DLP_LONG_RPT
-#define DLP_LONG_RPT 1  // rows per long-row tile (length imbalance wastes windows when > 1)
-#endif
-#ifndef DLP_SM_MAX_NA
-#define DLP_SM_MAX_NA 0  // rounds with at most this many active columns use step-major tiles (measured slower: off)
+#define DLP_WIN 64
 #endif
 #ifndef DLP_LABEL_WIN
-#define DLP_LABEL_WIN 48  // C-wide label rows staged per warp window
+#define DLP_LABEL_WIN 64  // C-wide label rows staged per warp window (>= DLP_WIN)
 #endif
 #ifndef DLP_HUB_WIN
 #define DLP_HUB_WIN 128
@@ -525,32 +519,24 @@ __device__ inline double finish_view(double s, double wall, const double* q, dou
     return fabs(__dsub_rn(fn, fu));
 }
 
-// Round geometry, set with the round's actions (every CTA's controller).
-// Two tile shapes:
-// * flat (many active columns): a tile holds rpt = 32 / C rows and lane
-//   (r, c) runs row r's sum for column c; a window stages the next kWin
-//   entries of the tile's concatenated rows, and a lane sums the part of its
-//   row inside the window.
-// * step-major (few active columns: na <= c_sm_max_na): rpt = 32 / na rows,
-//   lane (r, a) runs row r's sum for active column acol[a]; a window stages
-//   S consecutive entries of EVERY row of the tile so all lanes advance
-//   together (a certify round of one column packs 32 rows per warp instead of
-//   idling 31 lanes).  Label words are copied as one 8-byte word per entry
-//   when a single column is active (span 1), else as the whole C-wide row.  S
-//   is a multiple of the sum unroll U; slots past a row's end are staged as
-//   (w = 0, x = 0), which adds exactly nothing to s (s starts at +0.0 and is
-//   never -0.0), so the sums run in whole blocks of U.
-// The per-lane slot table and accumulate roles are computed once per round.
-constexpr int kQ = 2;  // window slots per gathering lane (step-major windows of <= 64 entries)
-constexpr int kWinW = 32 * kQ;
-// warp-private staging (doubles): kWinW weights, then the label words (at
-// least kWinW single words, or DLP_LABEL_WIN C-wide rows)
+// Warp-private staging (doubles): the window's weights, its label rows
+// (DLP_LABEL_WIN >= kWin C-wide rows) and the tile's row constants.  A warp
+// tile holds rpt = 32 / C rows (one row per tile for the long class): lane
+// (r, c) runs row r's sum for column c; a window stages the next kWin entries
+// of the tile's concatenated rows (entry-parallel gathers) and a lane sums
+// the part of its row inside the window.  (A step-major layout -- S entries
+// of every row per window so all lanes advance together -- and a software
+// pipeline across tiles were measured slower on C2 and its binary variant and
+// removed.)
+constexpr int kWinW = DLP_WIN;  // weight slots of a warp window
 constexpr int kRowConst = 96;  // per warp: (q0, q1) of each accumulate lane, w_all of each tile row
+constexpr int kLabelWin = DLP_LABEL_WIN > DLP_WIN ? DLP_LABEL_WIN : DLP_WIN;  // >= the window
 __host__ __device__ inline int warp_smem_doubles(int C) {
-    return kWinW + (DLP_LABEL_WIN * C > kWinW ? DLP_LABEL_WIN * C : kWinW) + kRowConst;
+    return kWinW + (kLabelWin * C > kWinW ? kLabelWin * C : kWinW) + kRowConst;
 }
 // the row constants of the tile, copied asynchronously with the first
-// window's label words (sq = the warp's row-constant area)
+// window's label words (sq = the warp's row-constant area); rows without a
+// ground-truth neighbour get (0, 0) without a load
 __device__ inline void tile_consts(const LPParams& P, const WarpTile& T, double* sq, int nrows, int ar, int ac,
                                    bool aact, unsigned long long pol) {
     const int lane = threadIdx.x & 31;
@@ -563,46 +549,6 @@ __device__ inline void tile_consts(const LPParams& P, const WarpTile& T, double*
         }
     }
     if (lane < nrows && T.em[lane]) cp_async8(sq + 64 + lane, P.wsum + T.u[lane], pol);
-}
-__constant__ int c_sm_max_na = DLP_SM_MAX_NA;
-struct TileGeo {
-    int flat, na, rpt, S, U, cmin, span;
-    int acol[kMaxCols];
-    unsigned char qr[kQ][32], qs[kQ][32];  // step-major: slot q of lane l -> tile row (32 = none), step
-    unsigned char ar[32], ac[32];          // accumulate role of lane l (ar = 32: none)
-};
-
-__device__ inline void set_geo(TileGeo& G, unsigned int act, int C, int xcap, int max_rows) {
-    int na = 0;
-    for (int c = 0; c < C; c++)
-        if ((act >> c) & 1u) G.acol[na++] = c;
-    if (na == 0) G.acol[na++] = 0;  // idle round (the loop is about to end)
-    G.flat = na > c_sm_max_na;
-    if (G.flat) {  // every column, identity roles
-        na = C;
-        for (int c = 0; c < C; c++) G.acol[c] = c;
-    }
-    G.na = na;
-    G.rpt = min(32 / na, max_rows);
-    G.cmin = na == 1 ? G.acol[0] : 0;
-    G.span = na == 1 ? 1 : C;
-    int we = xcap / G.span;
-    if (we > kWinW) we = kWinW;
-    const int per = we / G.rpt;  // steps per row that fit
-    G.U = per >= 4 ? 4 : 2;
-    const int S = per / G.U * G.U;
-    G.S = S < G.U ? G.U : S;  // rpt * S <= kWinW always holds for U = 2
-    for (int l = 0; l < 32; l++) {
-        for (int q = 0; q < kQ; q++) {
-            const int j = l + 32 * q;
-            const int r = j / G.S;
-            G.qr[q][l] = (unsigned char)(r < G.rpt ? r : 32);
-            G.qs[q][l] = (unsigned char)(j - r * G.S);
-        }
-        const int r = l / na;
-        G.ar[l] = (unsigned char)(r < G.rpt ? r : 32);
-        G.ac[l] = (unsigned char)G.acol[l - r * na];
-    }
 }
 
 // Round context shared by the tile routine.
@@ -836,93 +782,13 @@ __device__ void warp_tile_flat(const LPParams& P, const RoundCtx& R, ClaimCtx& K
     tile_expand(P, R, K, T, k0, nrows, ar, ch);
 }
 
-// Step-major tile (see TileGeo): S entries of every row per window, sums in
-// blocks of U over zero-padded row tails.
-template <int U>
-__device__ void warp_tile_sm(const LPParams& P, const RoundCtx& R, const TileGeo& G, ClaimCtx& K,
-                             BlockCounters& B, WarpTile& T, double* sw, double* sx, double* sq, long long k0,
-                             int nrows,
-                             unsigned long long pol, const TileMeta& m, int un, TileMeta* mn) {
-    const int C = P.C;
-    const int lane = threadIdx.x & 31;
-    const int S = G.S, span = G.span;
-    int maxlen;
-    tile_rows(P, R, B, T, k0, nrows, m, &maxlen);
-    __syncwarp();
-    const int ar = G.ar[lane], ac = G.ac[lane];
-    const bool aact = ar < nrows && ((T.em[ar] >> ac) & 1u);
-    const int len_a = aact ? T.len[ar] : 0;
-    const double fu = aact ? ld_keep(P.X + (long long)T.u[ar] * C + ac, pol) : 0.0;
-    tile_consts(P, T, sq, nrows, ar, ac, aact, pol);
-    *mn = load_meta(P, R, un);
-    RowS acc;
-    acc.init();
-    int vv[kQ];
-    double ww[kQ];
-    auto load_ids = [&](int wb) {
-#pragma unroll
-        for (int q = 0; q < kQ; q++) {
-            const int r = G.qr[q][lane];
-            if (r < nrows) {
-                const int e = wb + G.qs[q][lane];
-                if (e < T.len[r]) {
-                    const long long p = T.st[r] + e;
-                    vv[q] = __ldcs(P.vnbr + p);
-                    ww[q] = __ldcs(P.vw + p);
-                }
-            }
-        }
-    };
-    if (maxlen > 0) load_ids(0);
-    const double* xcol = P.X + G.cmin;
-    for (int wb = 0; wb < maxlen; wb += S) {
-#pragma unroll
-        for (int q = 0; q < kQ; q++) {
-            const int r = G.qr[q][lane];
-            if (r >= nrows) continue;
-            const int j = lane + 32 * q;
-            const int e = wb + G.qs[q][lane];
-            const int lr = T.len[r];
-            if (e < lr) {
-                sw[j] = ww[q];
-                if (span == 1)
-                    cp_async8(sx + j, xcol + (long long)vv[q] * C, pol);
-                else
-                    copy_label_row(sx + j * span, P.X + (long long)vv[q] * C, C, pol);
-            } else if (e - wb < ((lr - wb + U - 1) / U) * U) {  // pad the row's last block
-                sw[j] = 0.0;
-                for (int c = 0; c < span; c++) sx[j * span + c] = 0.0;
-            }
-        }
-        if (wb + S < maxlen) load_ids(wb + S);
-        cp_async_wait_all();
-        __syncwarp();
-        if (aact) {
-            const int hi = min(S, len_a - wb);
-            const double* w0p = sw + ar * S;
-            const double* x0p = sx + (ar * S) * span + (ac - G.cmin);
-            for (int t = 0; t < hi; t += U) acc.add_block<U>(w0p + t, x0p + t * span, span, fu);
-        }
-        __syncwarp();
-    }
-    if (maxlen == 0) {  // no window ran: the row constants' copies must still land
-        cp_async_wait_all();
-        __syncwarp();
-    }
-    const unsigned int ch = tile_finish(P, R, K, T, sq, k0, ar, ac, aact, acc.s, fu);
-    if (P.itlp) return;
-    if (!__any_sync(0xffffffffu, ch != 0)) return;
-    tile_expand(P, R, K, T, k0, nrows, ar, ch);
-}
-
 // Warp loop over the tiles of one row class: tile indices are grabbed two
 // ahead and row metadata one ahead (software pipeline), so a tile's
 // dependent chain of loads overlaps the previous tile's gathers.
-__device__ void warp_tiles(const LPParams& P, const RoundCtx& R, const TileGeo& G, ClaimCtx& K,
-                           BlockCounters& B, WarpTile& T, double* sw, double* sx, double* sq, unsigned int* grab,
-                           long long nitems, unsigned long long pol) {
+__device__ void warp_tiles(const LPParams& P, const RoundCtx& R, int per, ClaimCtx& K, BlockCounters& B,
+                           WarpTile& T, double* sw, double* sx, double* sq, unsigned int* grab, long long nitems,
+                           unsigned long long pol) {
     const int lane = threadIdx.x & 31;
-    const int per = G.rpt;
     if (nitems <= 0) return;
     unsigned int kr = 0;
     if (lane == 0) kr = atomicAdd(grab, (unsigned int)per);
@@ -937,12 +803,7 @@ __device__ void warp_tiles(const LPParams& P, const RoundCtx& R, const TileGeo& 
         const int un = lane < nrn ? R.W[kn + lane] : -1;
         if (lane == 0 && kn < nitems) kr = atomicAdd(grab, (unsigned int)per);
         TileMeta mn;
-        if (G.flat)
-            warp_tile_flat(P, R, K, B, T, sw, sx, sq, k, nr, pol, m, un, &mn);
-        else if (G.U == 4)
-            warp_tile_sm<4>(P, R, G, K, B, T, sw, sx, sq, k, nr, pol, m, un, &mn);
-        else
-            warp_tile_sm<2>(P, R, G, K, B, T, sw, sx, sq, k, nr, pol, m, un, &mn);
+        warp_tile_flat(P, R, K, B, T, sw, sx, sq, k, nr, pol, m, un, &mn);
         __syncwarp();
         if (kn >= nitems) break;
         k = kn;
@@ -1099,7 +960,6 @@ __device__ inline void gsync(LPCtl* ctl, unsigned int& target) { grid_sync(&ctl-
 __global__ void __launch_bounds__(kLpThreads, DLP_LP_MINB) k_lp_fused(LPParams P) {
     extern __shared__ double smem_dyn[];
     __shared__ ColState S;
-    __shared__ TileGeo s_geo, s_geo_l;  // short-row / long-row tile shapes
     __shared__ ClaimTargets s_ct;        // the round's claim targets
     __shared__ BlockCounters B;
     __shared__ WarpTile TT[kLpThreads / 32];
@@ -1178,8 +1038,6 @@ __global__ void __launch_bounds__(kLpThreads, DLP_LP_MINB) k_lp_fused(LPParams P
             decide_actions_act(S, P, nullptr, nullptr, 1);
         else
             decide_actions(S, P, nullptr, nullptr, 1);
-        set_geo(s_geo, S.fr_mask | S.cert_mask, C, wsm - kWinW - kRowConst, 32);
-        set_geo(s_geo_l, S.fr_mask | S.cert_mask, C, wsm - kWinW - kRowConst, DLP_LONG_RPT);
     }
     long long nel[3], ncur[3];
     for (int j = 0; j < 3; j++) {
@@ -1234,7 +1092,16 @@ __global__ void __launch_bounds__(kLpThreads, DLP_LP_MINB) k_lp_fused(LPParams P
 #endif
             if (prof) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(p_tw0));
             const unsigned long long tw0 = p_tw0;
-            if (n2c > 0) {
+            // hub rows: whole CTA per row in small rounds, where the longest row is
+            // the round's critical path; in big rounds (throughput-bound) they are
+            // single-row warp tiles like long rows, so no CTA idles at the window
+            // barriers (C2: 81.3 -> 79.8 ms)
+#ifndef DLP_HUB_CTA_ALWAYS
+            const bool hub_cta = !scan_mode;
+#else
+            constexpr bool hub_cta = true;
+#endif
+            if (n2c > 0 && hub_cta) {
                 for (;;) {  // hub rows: whole CTA per row (critical path first)
                     if (tid == 0) s_i[2] = (int)atomicAdd(&slot->grab[2], 1u);
                     __syncthreads();
@@ -1247,9 +1114,10 @@ __global__ void __launch_bounds__(kLpThreads, DLP_LP_MINB) k_lp_fused(LPParams P
             RoundCtx RL{W1, n0c, FR, CE, fm_cur, scan_mode, tmax};
             RoundCtx RS{W0, 0, FR, CE, fm_cur, scan_mode, tmax};
             if (prof) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tw1));
-            warp_tiles(P, RL, s_geo_l, K, B, T, sw, sx, sq, &slot->grab[1], n1c, pol);  // long rows
+            if (!hub_cta) warp_tiles(P, RH, 1, K, B, T, sw, sx, sq, &slot->grab[2], n2c, pol);
+            warp_tiles(P, RL, 1, K, B, T, sw, sx, sq, &slot->grab[1], n1c, pol);  // long rows: one per tile
             if (prof) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tw2));
-            warp_tiles(P, RS, s_geo, K, B, T, sw, sx, sq, &slot->grab[0], n0c, pol);  // short rows
+            warp_tiles(P, RS, 32 / C, K, B, T, sw, sx, sq, &slot->grab[0], n0c, pol);  // short rows
             if (prof) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tw3));
             if (prof) {  // warp-time per part of phase 1 (diagnostics)
                 atomicAdd(&ctl->prof[0], tw1 - tw0);
@@ -1258,8 +1126,8 @@ __global__ void __launch_bounds__(kLpThreads, DLP_LP_MINB) k_lp_fused(LPParams P
             }
         }
         if (K.claimed) atomicOr(&B.claimed, K.claimed);
-        if (K.c_nev) {  // lane (row, a) of every tile of the round works on column acol[a]
-            const int col = s_geo.ac[lane];
+        if (K.c_nev) {  // lane (row, c) of every tile works on column c = lane % C
+            const int col = lane % C;
             atomicAdd(&B.neval[col], (unsigned long long)K.c_nev);
             atomicAdd(&B.edges[col], K.c_edg);
             if (K.c_warn) atomicAdd(&B.warn[col], (unsigned long long)K.c_warn);
@@ -1422,8 +1290,6 @@ __global__ void __launch_bounds__(kLpThreads, DLP_LP_MINB) k_lp_fused(LPParams P
                     decide_actions_act(S, P, s_res, &s_claimed, 0);
                 else
                     decide_actions(S, P, s_res, &s_claimed, 0);
-                set_geo(s_geo, S.fr_mask | S.cert_mask, C, wsm - kWinW - kRowConst, 32);
-                set_geo(s_geo_l, S.fr_mask | S.cert_mask, C, wsm - kWinW - kRowConst, DLP_LONG_RPT);
             }
         }
         for (int j = 0; j < 3; j++) ncur[j] = s_cnt[j];
@@ -1520,10 +1386,6 @@ void lp_setup(Engine& E) {
     if (E.ncol > kMaxCols) throw CudaFailure(cudaErrorInvalidValue, "ncol > kMaxCols", __FILE__, __LINE__);
     E.lp_smem = std::max((size_t)(kLpThreads / 32) * warp_smem_doubles(E.ncol),
                          (size_t)2 * kHubWin * E.ncol) * sizeof(double);
-    if (const char* v = getenv("DLP_SM_MAX_NA")) {
-        int x = atoi(v);
-        DLP_CUDA_TRY(cudaMemcpyToSymbol(c_sm_max_na, &x, sizeof(int)));
-    }
     DLP_CUDA_TRY(cudaFuncSetAttribute(k_lp_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)E.lp_smem));
     if (const char* v = getenv("DLP_CARVEOUT"))  // shared-memory share of L1 (percent), tuning
         DLP_CUDA_TRY(cudaFuncSetAttribute(k_lp_fused, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(v)));
