@@ -228,3 +228,64 @@ def test_nccl_in_handle_world1(gpu_device, kind, mode):
                 (x.iterations, x.updates, x.max_change, x.converged, x.warnings), (t, c)
         assert lab.F.tobytes() == Fw.tobytes(), f"batch {t}: labels differ"
     g.close()
+
+
+def _engine_proc(rank, world, port, mode, q):
+    """One rank of a 2-process sharded engine run on the one GPU (gloo carries
+    the phase reductions and the row exchange between the processes)."""
+    sys.path.insert(0, os.path.dirname(HERE))
+    sys.path.insert(0, HERE)
+    try:
+        import torch.distributed as dist
+
+        from paper_2604_06596_b200.engine import EngineConfig, LabelState
+        from paper_2604_06596_b200.sharded import ShardedGraph, apply_batch_sharded, torch_collective
+
+        dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+        batches, ncls = _stream("blobs10" if mode != "rows" else "giant")
+        g = ShardedGraph(0, ncls, rank, world, torch_collective(), mode)
+        lab = LabelState()
+        reps = []
+        for b in batches:
+            lab, r = apply_batch_sharded(g, lab, b, EngineConfig(delta=1e-5))
+            r = r if isinstance(r, list) else [r]
+            reps.append([(x.iterations, x.updates, x.max_change, x.converged, x.warnings) for x in r])
+        F, _ = g.read_labels()
+        q.put((rank, reps, F, g.owned()))
+        g.close()
+        dist.destroy_process_group()
+    except Exception as e:  # pragma: no cover - surfaced by the parent
+        import traceback
+
+        q.put((rank, "error", f"{e!r}\n{traceback.format_exc()}", None))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["components", "rows"])
+def test_engine_two_processes_gloo(gpu_device, mode):
+    """The sharded ENGINE across two processes (world_size 2, gloo collective,
+    both ranks on the one GPU): global reports and merged labels bitwise equal
+    to the unsharded engine."""
+    from paper_2604_06596_b200.engine import EngineConfig
+    from paper_2604_06596_b200.sharded import merge_labels
+
+    batches, ncls = _stream("blobs10" if mode != "rows" else "giant")
+    want = _unsharded(batches, EngineConfig(delta=1e-5), ncls)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_engine_proc, args=(r, 2, port, mode, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    out = {}
+    for _ in range(2):
+        rank, reps, F, owned = q.get(timeout=600)
+        assert reps != "error", F
+        out[rank] = (reps, F, owned)
+    for p in ps:
+        p.join(timeout=120)
+    for t, (rw, _) in enumerate(want):
+        exp = [(a.iterations, a.updates, a.max_change, a.converged, a.warnings) for a in rw]
+        assert out[0][0][t] == exp and out[1][0][t] == exp, f"batch {t}"
+    F = merge_labels([(out[r][1], out[r][2]) for r in range(2)]) if mode != "rows" else out[0][1]
+    assert F.tobytes() == want[-1][1].tobytes()
