@@ -528,27 +528,39 @@ __device__ inline double finish_view(double s, double wall, const double* q, dou
 // of every row per window so all lanes advance together -- and a software
 // pipeline across tiles were measured slower on C2 and its binary variant and
 // removed.)
-constexpr int kWinW = DLP_WIN;  // weight slots of a warp window
-constexpr int kRowConst = 96;  // per warp: (q0, q1) of each accumulate lane, w_all of each tile row
+#ifndef DLP_RPL2
+#define DLP_RPL2 1  // short rows: two rows per lane (C >= 2)
+#endif
+#ifndef DLP_WIN2
+#define DLP_WIN2 128  // window of the two-rows-per-lane tiles
+#endif
+constexpr bool kRpl2 = DLP_RPL2;
+constexpr int kWin2 = DLP_WIN2;
+constexpr int kRpl2MaxC = 10;  // its staging (kWin2 x C label words) must fit two CTAs per SM
+constexpr int kWinW = DLP_WIN > DLP_WIN2 ? DLP_WIN : DLP_WIN2;  // weight slots of a warp window
+constexpr int kRowConst = 160;  // per warp: w_all of each tile row, (q0, q1) of each (lane, pass)
 constexpr int kLabelWin = DLP_LABEL_WIN > DLP_WIN ? DLP_LABEL_WIN : DLP_WIN;  // >= the window
 __host__ __device__ inline int warp_smem_doubles(int C) {
-    return kWinW + (kLabelWin * C > kWinW ? kLabelWin * C : kWinW) + kRowConst;
+    int lw = kLabelWin * C;
+    if (kRpl2 && C >= 2 && C <= kRpl2MaxC && kWin2 * C > lw) lw = kWin2 * C;
+    return kWinW + (lw > kWinW ? lw : kWinW) + kRowConst;
 }
 // the row constants of the tile, copied asynchronously with the first
 // window's label words (sq = the warp's row-constant area); rows without a
 // ground-truth neighbour get (0, 0) without a load
 __device__ inline void tile_consts(const LPParams& P, const WarpTile& T, double* sq, int nrows, int ar, int ac,
-                                   bool aact, unsigned long long pol) {
+                                   bool aact, unsigned long long pol, int q) {
     const int lane = threadIdx.x & 31;
+    double* sl = sq + 32 + 64 * q + 2 * lane;
     if (aact) {
         if (T.gtn[ar]) {
-            cp_async16(sq + 2 * lane, P.q01 + ((long long)T.u[ar] * P.C + ac) * 2, pol);
+            cp_async16(sl, P.q01 + ((long long)T.u[ar] * P.C + ac) * 2, pol);
         } else {
-            sq[2 * lane] = 0.0;
-            sq[2 * lane + 1] = 0.0;
+            sl[0] = 0.0;
+            sl[1] = 0.0;
         }
     }
-    if (lane < nrows && T.em[lane]) cp_async8(sq + 64 + lane, P.wsum + T.u[lane], pol);
+    if (q == 0 && lane < nrows && T.em[lane]) cp_async8(sq + lane, P.wsum + T.u[lane], pol);
 }
 
 // Round context shared by the tile routine.
@@ -617,13 +629,13 @@ __device__ inline int tile_rows(const LPParams& P, const RoundCtx& R, BlockCount
 // (row, column), count, and flag the columns that moved by more than delta.
 __device__ inline unsigned int tile_finish(const LPParams& P, const RoundCtx& R, ClaimCtx& K, const WarpTile& T,
                                           const double* sq, long long k0, int ar, int ac, bool aact, double s,
-                                          double fu) {
+                                          double fu, int q) {
     unsigned int ch = 0;
     if (aact) {
         const int u = T.u[ar];
         const int C = P.C;
         double val;
-        const double d = finish_view(s, sq[64 + ar], sq + 2 * (threadIdx.x & 31), fu, &val);
+        const double d = finish_view(s, sq[ar], sq + 32 + 64 * q + 2 * (threadIdx.x & 31), fu, &val);
         __stcs(P.Y + (R.ybase + k0 + ar) * C + ac, val);
         K.c_nev++;
         K.c_edg += (unsigned long long)T.lenf[ar];
@@ -643,9 +655,8 @@ __device__ inline unsigned int tile_finish(const LPParams& P, const RoundCtx& R,
 // themselves and their (unlabeled) neighbours -- ground-truth neighbours are
 // never eligible, so the view's entries are exactly the candidates.
 __device__ inline void tile_expand(const LPParams& P, const RoundCtx& R, ClaimCtx& K, WarpTile& T, long long k0,
-                                   int nrows, int ar, unsigned int ch) {
+                                   int nrows) {
     const int lane = threadIdx.x & 31;
-    if (ch) atomicOr(&T.chg[ar], ch);
     __syncwarp();
     const unsigned int mrow = lane < nrows ? T.chg[lane] : 0u;
     if (mrow) {
@@ -682,11 +693,16 @@ __device__ inline void tile_expand(const LPParams& P, const RoundCtx& R, ClaimCt
 // label rows by cp.async; lane (r, c) sums its row's part of each window in
 // stored order.  `un` is the next tile's row of this lane (-1 if none),
 // whose metadata is loaded into *mn mid-tile.
+template <int RPL, int WIN>
 __device__ void warp_tile_flat(const LPParams& P, const RoundCtx& R, ClaimCtx& K, BlockCounters& B, WarpTile& T,
                                double* sw, double* sx, double* sq, long long k0, int nrows, unsigned long long pol,
                                const TileMeta& m, int un, TileMeta* mn) {
+    // RPL rows per lane: lane (r, c) runs the sums of rows r and r + 32/C
+    // (RPL = 2, C >= 2), two independent chains per lane and twice the
+    // gathers in flight per warp.
     const int C = P.C;
     const int lane = threadIdx.x & 31;
+    const int rpt1 = 32 / C;
     int maxlen;
     const int total = tile_rows(P, R, B, T, k0, nrows, m, &maxlen);
     int incl = lane < nrows ? T.len[lane] : 0;
@@ -698,22 +714,30 @@ __device__ void warp_tile_flat(const LPParams& P, const RoundCtx& R, ClaimCtx& K
     }
     if (lane < nrows) T.off[lane] = incl - T.len[lane];
     __syncwarp();
-    const int ar = lane / C, ac = lane - ar * C;
-    const bool aact = ar < nrows && ((T.em[ar] >> ac) & 1u);
-    const double fu = aact ? ld_keep(P.X + (long long)T.u[ar] * C + ac, pol) : 0.0;
-    tile_consts(P, T, sq, nrows, ar, ac, aact, pol);
-    const int a_lo = aact ? T.off[ar] : 0, a_hi = aact ? T.off[ar] + T.len[ar] : 0;
+    const int ar0 = lane / C, ac = lane - ar0 * C;
+    int arq[RPL], a_lo[RPL], a_hi[RPL];
+    bool aact[RPL];
+    double fu[RPL];
+    RowS acc[RPL];
+#pragma unroll
+    for (int q = 0; q < RPL; q++) {
+        arq[q] = ar0 + q * rpt1;
+        aact[q] = ar0 < rpt1 && arq[q] < nrows && ((T.em[arq[q]] >> ac) & 1u);
+        fu[q] = aact[q] ? ld_keep(P.X + (long long)T.u[arq[q]] * C + ac, pol) : 0.0;
+        tile_consts(P, T, sq, nrows, arq[q], ac, aact[q], pol, q);
+        a_lo[q] = aact[q] ? T.off[arq[q]] : 0;
+        a_hi[q] = aact[q] ? T.off[arq[q]] + T.len[arq[q]] : 0;
+        acc[q].init();
+    }
     *mn = load_meta(P, R, un);  // next tile's metadata, consumed next iteration
-    RowS acc;
-    acc.init();
-    int vv[kWin / 32], rr[kWin / 32];
-    double ww[kWin / 32];
+    int vv[WIN / 32], rr[WIN / 32];
+    double ww[WIN / 32];
 #pragma unroll
-    for (int j = 0; j < kWin / 32; j++) rr[j] = -1;  // a tile whose rows have no unlabeled entry runs no window
+    for (int j = 0; j < WIN / 32; j++) rr[j] = -1;  // a tile whose rows have no unlabeled entry runs no window
     auto load_ids = [&](int wb) {
-        const int wn = min(kWin, total - wb);
+        const int wn = min(WIN, total - wb);
 #pragma unroll
-        for (int j = 0; j < kWin / 32; j++) {
+        for (int j = 0; j < WIN / 32; j++) {
             const int i = lane + 32 * j;
             rr[j] = -1;
             if (i < wn) {
@@ -727,23 +751,48 @@ __device__ void warp_tile_flat(const LPParams& P, const RoundCtx& R, ClaimCtx& K
         }
     };
     if (total > 0) load_ids(0);
-    for (int wb = 0; wb < total; wb += kWin) {
-        const int wn = min(kWin, total - wb);
+    for (int wb = 0; wb < total; wb += WIN) {
+        const int wn = min(WIN, total - wb);
 #pragma unroll
-        for (int j = 0; j < kWin / 32; j++) {
+        for (int j = 0; j < WIN / 32; j++) {
             if (rr[j] < 0) continue;
             const int i = lane + 32 * j;
             sw[i] = ww[j];
             copy_label_row(sx + i * C, P.X + (long long)vv[j] * C, C, pol);
         }
-        if (wb + kWin < total) load_ids(wb + kWin);
+        if (wb + WIN < total) load_ids(wb + WIN);
         cp_async_wait_all();
         __syncwarp();
-        if (aact) {
-            const int lo = max(a_lo, wb) - wb, hi = min(a_hi, wb + wn) - wb;
-            int t = lo;
-            for (; t + kAccUnroll <= hi; t += kAccUnroll) acc.add_block<kAccUnroll>(sw + t, sx + t * C + ac, C, fu);
-            for (; t < hi; t++) acc.add(sw[t], sx[t * C + ac], fu);
+        if (RPL == 1) {
+            if (aact[0]) {
+                const int lo = max(a_lo[0], wb) - wb, hi = min(a_hi[0], wb + wn) - wb;
+                int t = lo;
+                for (; t + kAccUnroll <= hi; t += kAccUnroll)
+                    acc[0].add_block<kAccUnroll>(sw + t, sx + t * C + ac, C, fu[0]);
+                for (; t < hi; t++) acc[0].add(sw[t], sx[t * C + ac], fu[0]);
+            }
+        } else {  // both rows' segments advance in the same loop: two chains per lane
+            int lo[RPL], n[RPL];
+#pragma unroll
+            for (int q = 0; q < RPL; q++) {
+                lo[q] = aact[q] ? max(a_lo[q], wb) - wb : 0;
+                n[q] = aact[q] ? max(0, min(a_hi[q], wb + wn) - wb - lo[q]) : 0;
+            }
+            int j = 0;
+            const int nb = min(n[0], n[1]);
+            for (; j + kAccUnroll <= nb; j += kAccUnroll) {
+#pragma unroll
+                for (int q = 0; q < RPL; q++)
+                    acc[q].add_block<kAccUnroll>(sw + lo[q] + j, sx + (lo[q] + j) * C + ac, C, fu[q]);
+            }
+#pragma unroll
+            for (int q = 0; q < RPL; q++) {
+                int t = lo[q] + j;
+                const int hi = lo[q] + n[q];
+                for (; t + kAccUnroll <= hi; t += kAccUnroll)
+                    acc[q].add_block<kAccUnroll>(sw + t, sx + t * C + ac, C, fu[q]);
+                for (; t < hi; t++) acc[q].add(sw[t], sx[t * C + ac], fu[q]);
+            }
         }
         __syncwarp();
     }
@@ -751,13 +800,21 @@ __device__ void warp_tile_flat(const LPParams& P, const RoundCtx& R, ClaimCtx& K
         cp_async_wait_all();
         __syncwarp();
     }
-    const unsigned int ch = tile_finish(P, R, K, T, sq, k0, ar, ac, aact, acc.s, fu);
+    unsigned int ch[RPL];
+#pragma unroll
+    for (int q = 0; q < RPL; q++)
+        ch[q] = tile_finish(P, R, K, T, sq, k0, arq[q], ac, aact[q], acc[q].s, fu[q], q);
     if (P.itlp) return;
-    if (!__any_sync(0xffffffffu, ch != 0)) return;
-    if (kExpandRegs && total <= kWin) {
+    unsigned int chany = 0;
+#pragma unroll
+    for (int q = 0; q < RPL; q++) chany |= ch[q];
+    if (!__any_sync(0xffffffffu, chany != 0)) return;
+#pragma unroll
+    for (int q = 0; q < RPL; q++)
+        if (ch[q]) atomicOr(&T.chg[arq[q]], ch[q]);
+    __syncwarp();
+    if (kExpandRegs && total <= WIN) {
         // single-window tile: the gathering lanes still hold the entries' ids
-        if (ch) atomicOr(&T.chg[ar], ch);
-        __syncwarp();
         const unsigned int mrow = lane < nrows ? T.chg[lane] : 0u;
         if (mrow) {
             K.claimed |= mrow;
@@ -768,7 +825,7 @@ __device__ void warp_tile_flat(const LPParams& P, const RoundCtx& R, ClaimCtx& K
                 claim(K, T.u[lane], mrow);
         }
 #pragma unroll
-        for (int j = 0; j < kWin / 32; j++) {
+        for (int j = 0; j < WIN / 32; j++) {
             if (rr[j] < 0) continue;
             const unsigned int mq = T.chg[rr[j]];
             if (!mq) continue;
@@ -779,7 +836,7 @@ __device__ void warp_tile_flat(const LPParams& P, const RoundCtx& R, ClaimCtx& K
         }
         return;
     }
-    tile_expand(P, R, K, T, k0, nrows, ar, ch);
+    tile_expand(P, R, K, T, k0, nrows);
 }
 
 // Warp loop over the tiles of one row class: tile indices are grabbed two
@@ -787,7 +844,7 @@ __device__ void warp_tile_flat(const LPParams& P, const RoundCtx& R, ClaimCtx& K
 // dependent chain of loads overlaps the previous tile's gathers.
 __device__ void warp_tiles(const LPParams& P, const RoundCtx& R, int per, ClaimCtx& K, BlockCounters& B,
                            WarpTile& T, double* sw, double* sx, double* sq, unsigned int* grab, long long nitems,
-                           unsigned long long pol) {
+                           unsigned long long pol, bool rpl2 = false) {
     const int lane = threadIdx.x & 31;
     if (nitems <= 0) return;
     unsigned int kr = 0;
@@ -803,7 +860,10 @@ __device__ void warp_tiles(const LPParams& P, const RoundCtx& R, int per, ClaimC
         const int un = lane < nrn ? R.W[kn + lane] : -1;
         if (lane == 0 && kn < nitems) kr = atomicAdd(grab, (unsigned int)per);
         TileMeta mn;
-        warp_tile_flat(P, R, K, B, T, sw, sx, sq, k, nr, pol, m, un, &mn);
+        if (rpl2)
+            warp_tile_flat<2, kWin2>(P, R, K, B, T, sw, sx, sq, k, nr, pol, m, un, &mn);
+        else
+            warp_tile_flat<1, kWin>(P, R, K, B, T, sw, sx, sq, k, nr, pol, m, un, &mn);
         __syncwarp();
         if (kn >= nitems) break;
         k = kn;
@@ -1117,7 +1177,9 @@ __global__ void __launch_bounds__(kLpThreads, DLP_LP_MINB) k_lp_fused(LPParams P
             if (!hub_cta) warp_tiles(P, RH, 1, K, B, T, sw, sx, sq, &slot->grab[2], n2c, pol);
             warp_tiles(P, RL, 1, K, B, T, sw, sx, sq, &slot->grab[1], n1c, pol);  // long rows: one per tile
             if (prof) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tw2));
-            warp_tiles(P, RS, 32 / C, K, B, T, sw, sx, sq, &slot->grab[0], n0c, pol);  // short rows
+            // short rows: 32/C rows per tile, or 2 x 32/C with two rows per lane
+            const bool rpl2 = kRpl2 && C >= 2 && C <= kRpl2MaxC;
+            warp_tiles(P, RS, rpl2 ? 2 * (32 / C) : 32 / C, K, B, T, sw, sx, sq, &slot->grab[0], n0c, pol, rpl2);
             if (prof) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tw3));
             if (prof) {  // warp-time per part of phase 1 (diagnostics)
                 atomicAdd(&ctl->prof[0], tw1 - tw0);

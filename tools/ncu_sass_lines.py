@@ -15,15 +15,18 @@ from collections import defaultdict
 
 
 def main(rep, lib, kname, srcname="lp.cu", top=40):
-    tmp = tempfile.mkdtemp()
-    subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(lib)], cwd=tmp, capture_output=True)
     cub = None
-    for f in os.listdir(tmp):
-        if f.endswith(".cubin"):
-            s = subprocess.run(["cuobjdump", "-sass", os.path.join(tmp, f)], capture_output=True, text=True).stdout
-            if kname in s:
-                cub = os.path.join(tmp, f)
-                break
+    if lib.endswith(".cubin"):
+        cub = lib
+    else:
+        tmp = tempfile.mkdtemp()
+        subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(lib)], cwd=tmp, capture_output=True)
+        for f in os.listdir(tmp):
+            if f.endswith(".cubin"):
+                s = subprocess.run(["cuobjdump", "-sass", os.path.join(tmp, f)], capture_output=True, text=True).stdout
+                if kname in s:
+                    cub = os.path.join(tmp, f)
+                    break
     dis = subprocess.run(["nvdisasm", "-g", "-c", cub], capture_output=True, text=True).stdout
     lines, fn, cur, ctx = {}, None, None, None
     for ln in dis.splitlines():
@@ -56,7 +59,8 @@ def main(rep, lib, kname, srcname="lp.cu", top=40):
         tot[0] += e
         tot[1] += s
     here = os.path.dirname(os.path.abspath(__file__))
-    src = open(os.path.join(here, "..", "paper_2604_06596_b200", "csrc", srcname)).read().split("\n")
+    srcpath = os.environ.get("NCU_SRC") or os.path.join(here, "..", "paper_2604_06596_b200", "csrc", srcname)
+    src = open(srcpath).read().split("\n")
     print(f"total warp-instructions {tot[0]:.4g}, stall samples {tot[1]}")
     print("## by context line (" + srcname + ")")
     for k, v in sorted(by_ctx.items(), key=lambda x: -x[1][0])[:top]:
