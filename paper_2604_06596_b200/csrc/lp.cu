@@ -529,7 +529,7 @@ __device__ inline double finish_view(double s, double wall, const double* q, dou
 // pipeline across tiles were measured slower on C2 and its binary variant and
 // removed.)
 #ifndef DLP_RPL2
-#define DLP_RPL2 1  // short rows: two rows per lane (C >= 2)
+#define DLP_RPL2 0  // short rows: two rows per lane (C >= 2); measured slower on C2 (100.5 vs 81.0 ms), off
 #endif
 #ifndef DLP_WIN2
 #define DLP_WIN2 128  // window of the two-rows-per-lane tiles
