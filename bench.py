@@ -145,7 +145,15 @@ def make_stream(cfg, device):
             edges = streams.knn_graph_grid3d(bl.x, cfg["k"])
         else:
             bl = streams.make_blobs(cfg["n"], cfg["dim"], cfg["classes"], cfg["seed"])
-            edges = streams.knn_graph_torch64(bl.x, cfg["k"], device=device or "cpu")
+            if cfg["n"] > 2_000_000 and device:
+                # 10M+ points: this repo's tensor-core k-NN (exact edge set; a torch fp64
+                # GEMM + top-k would need 8n bytes per query row).  Only the B200 arm
+                # runs these configs (no CPU reference at this size).
+                from paper_2604_06596_b200.knn import FeatureMatrix, knn_graph
+
+                edges = knn_graph(FeatureMatrix(bl.x), cfg["k"], device=int(device.split(":")[-1]))
+            else:
+                edges = streams.knn_graph_torch64(bl.x, cfg["k"], device=device or "cpu")
         gt = streams.stratified_seeds(bl.classes, cfg["seed_frac"], cfg["seed"])
         fi, fg, fd = cfg["fractions"]
         phases = None

@@ -75,12 +75,18 @@ constexpr int kAccUnroll = DLP_ACC_UNROLL;  // ordered-sum loop unroll
 constexpr bool kExpandRegs = DLP_EXPAND_REGS;  // expand single-window tiles from the gather registers
 constexpr int kWin = DLP_WIN;   // row entries per warp window
 constexpr int kHubWin = DLP_HUB_WIN;  // row entries per CTA window (hub rows)
-constexpr int kLongRow = 96;    // rows longer than this are warp tiles of their own
+#ifndef DLP_LONG_ROW_DEFAULT
+#define DLP_LONG_ROW_DEFAULT 96
+#endif
+constexpr int kLongRow = DLP_LONG_ROW_DEFAULT;  // rows longer than this are warp tiles of their own
 #ifndef DLP_HUB_ROW_DEFAULT
 #define DLP_HUB_ROW_DEFAULT 512
 #endif
 constexpr int kHubRow = DLP_HUB_ROW_DEFAULT;  // rows longer than this are evaluated by a whole CTA
-constexpr int kScanRatio = 64;  // rounds with >= n/64 rows expand by atomicOr + compaction
+#ifndef DLP_SCAN_RATIO
+#define DLP_SCAN_RATIO 64
+#endif
+constexpr int kScanRatio = DLP_SCAN_RATIO;  // rounds with >= n/64 rows expand by atomicOr + compaction
 
 enum { PH_FRONTIER = 0, PH_DONE = 2 };
 enum { CLS_SHORT = 0, CLS_LONG = 1, CLS_HUB = 2 };
