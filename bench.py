@@ -198,6 +198,11 @@ class ClockSampler:
                 ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "200",
                  "-i", str(self.index)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             threading.Thread(target=self._read, daemon=True).start()
+            # nvidia-smi's start-up (NVML init) stalls the device for tens of ms:
+            # let it finish before the timed region begins
+            t_end = time.time() + 5.0
+            while not self.lines and time.time() < t_end:
+                time.sleep(0.05)
         except Exception:
             self.proc = None
 

@@ -84,9 +84,9 @@ constexpr int kLongRow = DLP_LONG_ROW_DEFAULT;  // rows longer than this are war
 #endif
 constexpr int kHubRow = DLP_HUB_ROW_DEFAULT;  // rows longer than this are evaluated by a whole CTA
 #ifndef DLP_SCAN_RATIO
-#define DLP_SCAN_RATIO 64
+#define DLP_SCAN_RATIO 16
 #endif
-constexpr int kScanRatio = DLP_SCAN_RATIO;  // rounds with >= n/64 rows expand by atomicOr + compaction
+constexpr int kScanRatio = DLP_SCAN_RATIO;  // rounds with >= n/16 rows: expand by atomicOr + compaction, hubs as warp tiles (64: +4%)
 
 enum { PH_FRONTIER = 0, PH_DONE = 2 };
 enum { CLS_SHORT = 0, CLS_LONG = 1, CLS_HUB = 2 };

@@ -2,7 +2,8 @@
 //
 // jacobi_step       kernels/_csr.pyx:61-91   (evaluate, do not commit)
 // gauss_seidel_step kernels/_csr.pyx:94-111  (sequential, in place)
-// jacobi_run        kernels/_csr.pyx:114-197 (fused frontier loop)
+// jacobi_run        kernels/_csr.pyx:114-197 (fused frontier loop; every
+//                   round on the device in one cooperative launch)
 //
 // These operate on a caller-supplied CSR (int64 indptr/indices, fp64
 // weights, int8 gt) exactly as the reference backend does, so the
@@ -75,42 +76,89 @@ struct PlugCtl {
     unsigned long long warnings;
 };
 
-__global__ void k_plug_commit(const long long* indptr, const long long* indices, const long long* cur, long long ncur,
-                              const double* vals, const double* deltas, double* f, const unsigned char* elig,
-                              const long long* iso_first, int* in_next, long long* nxt, PlugCtl* ctl, double delta) {
-    double lmax = 0.0;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < ncur; i += (long long)gridDim.x * blockDim.x) {
-        long long u = cur[i];
-        double d = deltas[i];
-        f[u] = vals[i];
-        if (d < 0.0) {
-            atomicAdd(&ctl->warnings, 1ULL);
-            continue;
+// jacobi_run as ONE cooperative launch: the rounds of _csr.pyx:155-194 run
+// on the device (step, commit, post separated by grid barriers; the round
+// bookkeeping is done by thread 0 of block 0 between them), so the host
+// neither synchronises nor launches per round.  Same kernels' bodies as the
+// per-round launches above.
+struct PlugRun {
+    PlugCtl ctl;                 // per-round counters (reset every round)
+    long long cur_len, iterations, updates;
+    unsigned long long warnings;
+    double max_change;
+    int parity;                  // which list holds the current frontier
+    unsigned int bar;            // grid barrier
+};
+
+__global__ void k_plug_run(const long long* indptr, const long long* indices, const double* weights,
+                           const signed char* gt, double* f, unsigned char* elig, long long* iso, int* in_next,
+                           long long* la, long long* lb, double* vals, double* dels, PlugRun* R, double delta,
+                           long long max_iters, long long n) {
+    unsigned int target = 0;
+    const long long gtid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const long long gth = (long long)gridDim.x * blockDim.x;
+    for (;;) {
+        const long long cur_len = *(volatile long long*)&R->cur_len;
+        const long long it = *(volatile long long*)&R->iterations;
+        if (cur_len <= 0 || it >= max_iters) break;
+        const int par = *(volatile int*)&R->parity;
+        long long* cur = par ? lb : la;
+        long long* nxt = par ? la : lb;
+        for (long long i = gtid; i < cur_len; i += gth) {  // evaluate (k_plug_step)
+            const long long u = cur[i];
+            double v;
+            const double d = plug_eval(indptr, indices, weights, gt, f, u, &v);
+            vals[i] = v;
+            dels[i] = d;
+            if (d < 0.0) atomicMin((unsigned long long*)&iso[u], (unsigned long long)i);
         }
-        lmax = fmax(lmax, d);
-        if (d > delta) {
-            if (elig[u] && iso_first[u] > i) plug_claim(in_next, nxt, &ctl->next, u);
-            for (long long e = indptr[u]; e < indptr[u + 1]; e++) {
-                long long v = indices[e];
-                if (elig[v] && iso_first[v] > i) plug_claim(in_next, nxt, &ctl->next, v);
+        grid_sync(&R->bar, target);
+        double lmax = 0.0;  // commit + expand (k_plug_commit)
+        for (long long i = gtid; i < cur_len; i += gth) {
+            const long long u = cur[i];
+            const double d = dels[i];
+            f[u] = vals[i];
+            if (d < 0.0) {
+                atomicAdd(&R->ctl.warnings, 1ULL);
+                continue;
+            }
+            lmax = fmax(lmax, d);
+            if (d > delta) {
+                if (elig[u] && iso[u] > i) plug_claim(in_next, nxt, &R->ctl.next, u);
+                for (long long e = indptr[u]; e < indptr[u + 1]; e++) {
+                    const long long v = indices[e];
+                    if (elig[v] && iso[v] > i) plug_claim(in_next, nxt, &R->ctl.next, v);
+                }
             }
         }
-    }
-    if (lmax > 0.0) atomic_max_nonneg(&ctl->rmax, lmax);
-}
-
-__global__ void k_plug_post(const long long* cur, long long ncur, const double* deltas, unsigned char* elig,
-                            long long* iso_first, const long long* nxt, const PlugCtl* ctl, int* in_next) {
-    long long nn = (long long)ctl->next;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < ncur; i += (long long)gridDim.x * blockDim.x) {
-        if (deltas[i] < 0.0) {
-            long long u = cur[i];
-            elig[u] = 0;
-            iso_first[u] = 0x7fffffffffffffffLL;
+        if (lmax > 0.0) atomic_max_nonneg(&R->ctl.rmax, lmax);
+        grid_sync(&R->bar, target);
+        const long long nn = (long long)*(volatile unsigned long long*)&R->ctl.next;  // post (k_plug_post)
+        for (long long i = gtid; i < cur_len; i += gth) {
+            if (dels[i] < 0.0) {
+                const long long u = cur[i];
+                elig[u] = 0;
+                iso[u] = 0x7fffffffffffffffLL;
+            }
         }
+        for (long long i = gtid; i < nn; i += gth) in_next[nxt[i]] = 0;
+        grid_sync(&R->bar, target);
+        if (gtid == 0) {  // round bookkeeping (the host loop's, _csr.pyx:192-194)
+            R->updates += cur_len;
+            R->iterations += 1;
+            union { unsigned long long u; double d; } cv;
+            cv.u = R->ctl.rmax;
+            R->max_change = cv.d;
+            R->warnings += R->ctl.warnings;
+            R->parity ^= 1;
+            R->cur_len = nn;
+            R->ctl.next = 0;
+            R->ctl.rmax = 0;
+            R->ctl.warnings = 0;
+        }
+        grid_sync(&R->bar, target);
     }
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nn; i += (long long)gridDim.x * blockDim.x)
-        in_next[nxt[i]] = 0;
+    (void)n;
 }
 
 __global__ void k_fill_ll(long long* p, long long n, long long v) {
@@ -215,36 +263,40 @@ extern "C" int dlp_jacobi_run(const int64_t* indptr, const int64_t* indices, con
         Tmp<long long> la(lcap, st), lb(lcap, st), iso(n + 1, st);
         Tmp<double> vals(lcap, st), dels(lcap, st);
         Tmp<int> in_next(n + 1, st);
-        Tmp<PlugCtl> ctl(1, st);
         DLP_CUDA_TRY(cudaMemsetAsync(in_next.p, 0, (n + 1) * sizeof(int), st));
         k_fill_ll<<<blocks_for(n + 1), kBlock, 0, st>>>(iso.p, n + 1, 0x7fffffffffffffffLL);
         if (nf) DLP_CUDA_TRY(cudaMemcpyAsync(la.p, frontier_init, nf * sizeof(long long), cudaMemcpyHostToDevice, st));
-        long long* cur = la.p;
-        long long* nxt = lb.p;
-        long long cur_len = nf, iterations = 0, updates = 0;
-        double max_change = 0.0;
-        PlugCtl h{};
-        unsigned long long warnings = 0;
-        while (cur_len > 0 && iterations < max_iters) {
-            DLP_CUDA_TRY(cudaMemsetAsync(ctl.p, 0, sizeof(PlugCtl), st));
-            int g = blocks_for(cur_len);
-            k_plug_step<<<g, kBlock, 0, st>>>(d_ip->p, d_ix->p, d_w->p, d_gt->p, d_f->p, cur, cur_len, vals.p, dels.p,
-                                              iso.p);
-            k_plug_commit<<<g, kBlock, 0, st>>>(d_ip->p, d_ix->p, cur, cur_len, vals.p, dels.p, d_f->p, d_el->p, iso.p,
-                                                in_next.p, nxt, ctl.p, delta);
-            k_plug_post<<<blocks_for(std::max<long long>(cur_len, n)), kBlock, 0, st>>>(cur, cur_len, dels.p, d_el->p,
-                                                                                       iso.p, nxt, ctl.p, in_next.p);
-            DLP_CUDA_TRY(cudaMemcpyAsync(&h, ctl.p, sizeof(PlugCtl), cudaMemcpyDeviceToHost, st));
-            DLP_CUDA_TRY(cudaStreamSynchronize(st));
-            updates += cur_len;
-            iterations++;
-            union { unsigned long long u; double d; } cv;
-            cv.u = h.rmax;
-            max_change = cv.d;
-            warnings += h.warnings;
-            std::swap(cur, nxt);
-            cur_len = (long long)h.next;
+        // the whole loop on the device: one cooperative launch
+        Tmp<PlugRun> run(1, st);
+        PlugRun h0{};
+        h0.cur_len = nf;
+        DLP_CUDA_TRY(cudaMemcpyAsync(run.p, &h0, sizeof(PlugRun), cudaMemcpyHostToDevice, st));
+        static int grid = 0;
+        if (!grid) {
+            int dev = 0, sms = 0, occ = 0;
+            DLP_CUDA_TRY(cudaGetDevice(&dev));
+            DLP_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+            DLP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_plug_run, kBlock, 0));
+            grid = sms * std::max(1, std::min(occ, 4));
         }
+        long long max_it = max_iters;
+        double dl = delta;
+        long long nn = n;
+        long long *ip = d_ip->p, *ix = d_ix->p, *isop = iso.p, *lap = la.p, *lbp = lb.p;
+        double *wp = d_w->p, *fp = d_f->p, *vp = vals.p, *dp = dels.p;
+        signed char* gp = d_gt->p;
+        unsigned char* ep = d_el->p;
+        int* inp = in_next.p;
+        PlugRun* rp = run.p;
+        void* args[] = {&ip, &ix, &wp, &gp, &fp, &ep, &isop, &inp, &lap, &lbp, &vp, &dp, &rp, &dl, &max_it, &nn};
+        DLP_CUDA_TRY(cudaLaunchCooperativeKernel((void*)k_plug_run, dim3(grid), dim3(kBlock), args, 0, st));
+        PlugRun h{};
+        DLP_CUDA_TRY(cudaMemcpyAsync(&h, run.p, sizeof(PlugRun), cudaMemcpyDeviceToHost, st));
+        DLP_CUDA_TRY(cudaStreamSynchronize(st));
+        const long long cur_len = h.cur_len, iterations = h.iterations, updates = h.updates;
+        const double max_change = h.max_change;
+        const unsigned long long warnings = h.warnings;
+        long long* cur = h.parity ? lb.p : la.p;
         std::vector<long long> left(cur_len);
         if (cur_len) DLP_CUDA_TRY(cudaMemcpyAsync(left.data(), cur, cur_len * sizeof(long long), cudaMemcpyDeviceToHost, st));
         if (n) {
