@@ -122,12 +122,15 @@ def load_stream_npz(path):
     from paper_2604_06596_b200.batch import BatchUpdate
 
     z = np.load(path)
-    io, eo, do = z["io"], z["eo"], z["do"]
-    batches = [BatchUpdate(t=t, insert_ids=z["ids"][io[t]:io[t + 1]], insert_gt=z["gt"][io[t]:io[t + 1]],
-                           edge_owner=z["own"][eo[t]:eo[t + 1]], edge_other=z["oth"][eo[t]:eo[t + 1]],
-                           edge_w=z["w"][eo[t]:eo[t + 1]], deletes=z["dels"][do[t]:do[t + 1]])
+    # every z[...] access re-reads the whole array: load each one once (slicing a
+    # fresh full copy per batch kept ~100 copies alive)
+    a = {k: z[k] for k in ("ids", "gt", "own", "oth", "w", "dels", "io", "eo", "do", "classes")}
+    io, eo, do = a["io"], a["eo"], a["do"]
+    batches = [BatchUpdate(t=t, insert_ids=a["ids"][io[t]:io[t + 1]], insert_gt=a["gt"][io[t]:io[t + 1]],
+                           edge_owner=a["own"][eo[t]:eo[t + 1]], edge_other=a["oth"][eo[t]:eo[t + 1]],
+                           edge_w=a["w"][eo[t]:eo[t + 1]], deletes=a["dels"][do[t]:do[t + 1]])
                for t in range(len(io) - 1)]
-    return batches, z["classes"]
+    return batches, a["classes"]
 
 
 def make_stream(cfg, device):

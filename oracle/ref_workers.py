@@ -39,11 +39,12 @@ def load_stream(path):
     """Batches of a bench stream cache (.npz written by bench.make_stream) as
     plain tuples (t, ids, gt, owner, other, w, dels)."""
     z = np.load(path)
-    io, eo, do = z["io"], z["eo"], z["do"]
+    a = {k: z[k] for k in ("ids", "gt", "own", "oth", "w", "dels", "io", "eo", "do")}  # one read per array
+    io, eo, do = a["io"], a["eo"], a["do"]
     out = []
     for t in range(len(io) - 1):
-        out.append((t, z["ids"][io[t]:io[t + 1]], z["gt"][io[t]:io[t + 1]], z["own"][eo[t]:eo[t + 1]],
-                    z["oth"][eo[t]:eo[t + 1]], z["w"][eo[t]:eo[t + 1]], z["dels"][do[t]:do[t + 1]]))
+        out.append((t, a["ids"][io[t]:io[t + 1]], a["gt"][io[t]:io[t + 1]], a["own"][eo[t]:eo[t + 1]],
+                    a["oth"][eo[t]:eo[t + 1]], a["w"][eo[t]:eo[t + 1]], a["dels"][do[t]:do[t + 1]]))
     return out
 
 

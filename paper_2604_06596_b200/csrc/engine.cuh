@@ -220,6 +220,7 @@ struct Engine {
     DevArray<double> log_w, log_w2;
     // batch staging -------------------------------------------------------
     PinnedArray<unsigned char> h_stage, h_stage2;  // batch staging (two slots: ingestion pipeline)
+    PinnedArray<double> h_readout;                 // label read-out bounce buffer (pinned: full-speed D2H)
     DevArray<unsigned char> d_stage, d_stage2;
     cudaStream_t cst = nullptr;   // copy stream of the ingestion pipeline
     cudaEvent_t cev = nullptr;    // staged copy complete
