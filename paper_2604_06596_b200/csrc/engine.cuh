@@ -252,7 +252,7 @@ struct Engine {
     void* nccl = nullptr;      // ncclComm_t of a sharded engine (dlp_shard_nccl), else null
     DevArray<unsigned long long> comm_buf, rows_send, rows_recv;  // NCCL staging (device)  // cusolverDnHandle_t of the harmonic oracle (created on first use)
     int lp_cert_hold = 1 << 30;  // certify alignment: max rounds a certify waits (DLP_CERT_HOLD)
-    int l2_mode = 1;            // label L2 residency: 0 none, 1 persisting carve-out, 2 + access window
+    int l2_mode = 0;            // label L2 residency: 0 none (default: C2 -0.8%, C4 -4% vs 1), 1 persisting carve-out, 2 + access window
     size_t l2_persist = 0;      // persisting L2 carve-out (bytes)
     size_t l2_window_max = 0;
     DevArray<unsigned long long> lp_trace;
