@@ -452,7 +452,7 @@ def main():
     ap.add_argument("--no-itlp", action="store_true", help="skip the ItLP comparison leg")
     ap.add_argument("--no-readback", action="store_true", help="skip the e2e label read-back leg")
     ap.add_argument("--replicas", action="store_true", help="N > 1: independent replicas instead of sharding")
-    ap.add_argument("--shard-mode", default="components", choices=["components", "rows"],
+    ap.add_argument("--shard-mode", default="components", choices=["components", "rows", "components_hash"],
                     help="N > 1: shard connected components, or partition rows (giant component)")
     ap.add_argument("--ref-steps", type=int, default=5, help="reference arm: timed batches (bounded sample)")
     ap.add_argument("--make-handoff", action="store_true",
@@ -516,15 +516,25 @@ def main():
     # (sharded.py; phase bookkeeping reduced with NCCL); --replicas runs N
     # independent copies instead.
     sharded = world > 1 and not args.replicas
+    # over NCCL the engines run every exchange on their own communicator (device
+    # buffers, no Python in the loop); gloo (CPU protocol checks) uses the host
+    # collective.  DYNLP_BENCH_HOST_COLLECTIVE=1 forces the host path.
+    nccl = sharded and dist.get_backend() == "nccl" and not os.environ.get("DYNLP_BENCH_HOST_COLLECTIVE")
     if sharded:
-        from paper_2604_06596_b200.sharded import ShardedGraph, apply_batch_sharded, torch_collective
+        from paper_2604_06596_b200.sharded import (ShardedGraph, apply_batch_sharded, nccl_unique_id,
+                                                   torch_collective)
 
-        nccl = dist.get_backend() == "nccl"
-        coll = torch_collective(device=device if nccl else None)
+        coll = None if nccl else torch_collective(device=device if dist.get_backend() == "nccl" else None)
 
     def new_graph():
         if sharded:
-            return ShardedGraph(local, max(2, cfg["classes"]), rank, world, coll, args.shard_mode), LabelState()
+            if nccl:  # a fresh communicator per engine (the id travels over the process group)
+                obj = [nccl_unique_id() if rank == 0 else None]
+                dist.broadcast_object_list(obj, src=0)
+                g = ShardedGraph(local, max(2, cfg["classes"]), rank, world, None, args.shard_mode, nccl_id=obj[0])
+            else:
+                g = ShardedGraph(local, max(2, cfg["classes"]), rank, world, coll, args.shard_mode)
+            return g, LabelState()
         return DynamicGraph(local, num_classes=max(2, cfg["classes"])), LabelState()
 
     def step(g, lab, b):
@@ -666,10 +676,10 @@ def main():
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": cfg["desc"], "points": cfg["n"], "timed_batches": f"t={t0}..{T - 1}",
                    "label_columns": ncol, "delta": delta,
-                   "parallelism": ((f"component-sharded x{world} (NCCL phase all-reduce)"
-                                    if args.shard_mode == "components" else
-                                    f"row-partitioned x{world} (per-round NCCL row all-gather)") if sharded
-                                   else f"replicas x{world}"),
+                   "parallelism": ((f"component-sharded x{world} (LPT placement, NCCL in the engine)"
+                                    if args.shard_mode != "rows" else
+                                    f"row-partitioned x{world} (per-round NCCL all-gather of packed rows)")
+                                   if sharded else f"replicas x{world}"),
                    "l2": "no flush: each batch's working set (adjacency pool, edge log, label and staging "
                          "columns) exceeds the 126 MB L2"},
         "edges_per_s": edges / (ms_value * K * 1e-3),
