@@ -63,14 +63,6 @@ __device__ inline double lds64(const double* p) {
 // keep every product and sum un-contracted, matching the compiled CPU kernel
 // (scalar SSE2 mulsd/addsd, no FMA).
 // ---------------------------------------------------------------------------
-// acc += v (round to nearest) when c; a predicated add in the SASS, so the
-// skipped sums cost one issue slot and no select
-__device__ inline void dadd_if(double& acc, double v, bool c) {
-    asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q add.rn.f64 %0, %0, %1;\n\t}"
-        : "+d"(acc)
-        : "d"(v), "r"((int)c));
-}
-
 struct RowAcc {
     double w_all, w0, w1, s;
     __device__ inline void init() { w_all = w0 = w1 = s = 0.0; }
@@ -83,80 +75,6 @@ struct RowAcc {
             w1 = __dadd_rn(w1, w);
         else
             s = __dadd_rn(s, __dmul_rn(__dsub_rn(fv, fu), w));
-    }
-    // same, with x = the NaN-boxed label word of the neighbour.  A sum that
-    // does not take this entry is left alone, which is the same as adding
-    // +0.0 (the sums are never -0.0: they start at +0.0 and a sum that
-    // cancels to zero rounds to +0.0).  Default: branch on the rare
-    // ground-truth entries (~12 instructions per unlabeled entry, measured
-    // fastest); -DDLP_SUMS_SELECT adds a selected +0.0 to every sum,
-    // -DDLP_SUMS_PRED predicates the three class-dependent adds.
-    __device__ inline void add_boxed(double w, double x, double fu) {
-        const bool gt = is_boxed(x);
-        w_all = __dadd_rn(w_all, w);
-#if defined(DLP_SUMS_SELECT)
-        const double p = __dmul_rn(__dsub_rn(x, fu), w);
-        const int cls = boxed_class(x);
-        w0 = __dadd_rn(w0, (gt && cls == 0) ? w : 0.0);
-        w1 = __dadd_rn(w1, (gt && cls == 1) ? w : 0.0);
-        s = __dadd_rn(s, gt ? 0.0 : p);
-#elif defined(DLP_SUMS_PRED)
-        const double p = __dmul_rn(__dsub_rn(x, fu), w);
-        const int c1 = __double2loint(x) & 1;
-        dadd_if(s, p, !gt);
-        dadd_if(w0, w, gt && !c1);
-        dadd_if(w1, w, gt && c1);
-#else
-        if (!gt) {
-            s = __dadd_rn(s, __dmul_rn(__dsub_rn(x, fu), w));
-        } else if (__double2loint(x) & 1) {
-            w1 = __dadd_rn(w1, w);
-        } else {
-            w0 = __dadd_rn(w0, w);
-        }
-#endif
-    }
-    // B consecutive entries (x strided by xs), same operations and order as
-    // B calls of add_boxed
-    template <int B>
-    __device__ inline void add_boxed_block(const double* w, const double* x, int xs, double fu) {
-#ifndef DLP_BLOCK_BRANCH
-        // s takes a selected +0.0 for ground-truth entries (no per-entry
-        // branch, so the block's terms overlap); w0 / w1 are updated in one
-        // rarely taken branch per block, in entry order
-        double wv[B], xv[B], pv[B];
-        bool any = false;
-#pragma unroll
-        for (int j = 0; j < B; j++) {
-            wv[j] = w[j];
-            xv[j] = x[j * xs];
-        }
-#pragma unroll
-        for (int j = 0; j < B; j++) {
-            const bool gt = is_boxed(xv[j]);
-            any |= gt;
-            const double p = __dmul_rn(__dsub_rn(xv[j], fu), wv[j]);
-            pv[j] = gt ? 0.0 : p;
-        }
-#pragma unroll
-        for (int j = 0; j < B; j++) {
-            w_all = __dadd_rn(w_all, wv[j]);
-            s = __dadd_rn(s, pv[j]);
-        }
-        if (any) {
-#pragma unroll
-            for (int j = 0; j < B; j++)
-                if (is_boxed(xv[j])) {
-                    if (__double2loint(xv[j]) & 1)
-                        w1 = __dadd_rn(w1, wv[j]);
-                    else
-                        w0 = __dadd_rn(w0, wv[j]);
-                }
-        }
-#else
-#pragma unroll
-        for (int j = 0; j < B; j++) add_boxed(w[j], x[j * xs], fu);
-#endif
     }
     // returns |fn - fu| or -1 for the isolated sentinel (value 0.5)
     __device__ inline double finish(double fu, double* out_val) const {

@@ -12,7 +12,7 @@
 //   per-vertex update kernels/_csr.pyx:24-58 (RowAcc in common.cuh)
 //   ItLP              baselines.py:190-233 (full sweeps over the active set)
 //
-// B200 design
+// B200 design (DESIGN.md section 4.1)
 // * Fused label columns.  The C one-vs-rest columns (C = 1 for binary) run in
 //   lockstep global rounds; each column follows its own reference state
 //   machine (frontier rounds -> certify -> ...), so per-column results are
@@ -20,23 +20,18 @@
 //   the union of the columns' frontiers (or the eligible list when a column
 //   certifies); every row is read ONCE per round for all columns and one
 //   gather of X[v*C .. v*C+C) serves every column.
-// * Two row classes.  Short rows (<= kLongRow entries, the bulk of a kNN
-//   graph) are evaluated warp-independently: a warp grabs 32/C rows, lane
-//   (row, column) walks its row in stored order -- the reference's sequential
-//   fp64 summation -- with kUnroll entries in flight (independent id/weight
-//   loads, then independent label gathers, then the ordered sums).  No CTA
-//   barrier is involved, so warps overlap each other's memory latency.
-//   Long rows (kNN hubs reach thousands of entries) are evaluated by a whole
-//   CTA: window by window the CTA gathers the entries and precomputes the
-//   independent product terms (f[v]-fu)*w in parallel into shared memory,
-//   then one thread per column runs the ordered dependent sums.
-// * Cache policy.  Adjacency (ids, weights) and the compact staging buffer
-//   are streamed (evict-first); label reads and commits carry an L2
-//   evict_last policy so the C-wide label vectors stay L2-resident while the
-//   adjacency streams through.
+// * The LP view (k_lp_view, per batch, cached per row): each row's unlabeled
+//   neighbours and its row constants w_all and w0/w_all, w1/w_all per column,
+//   so the sweeps run only the s chain of _update_one in the reference's order.
+// * Row classes by view length: short rows (32/C per warp tile), long rows
+//   (one per warp tile), hub rows (a whole CTA per row in small rounds, where
+//   the longest row is the critical path; warp tiles in big rounds).  A warp
+//   tile gathers entry-parallel into warp-private shared memory (64-entry
+//   windows, ids one window ahead, label rows by cp.async) and lane
+//   (row, column) runs its row's sum in stored order.
 // * Jacobi commit: phase 1 writes new values to a compact staging buffer
 //   (indexed by work item), phase 2 copies them into X; two grid-wide
-//   barriers per round.
+//   barriers per round, the controller replayed by every CTA.
 #include <cooperative_groups.h>
 
 #include <algorithm>

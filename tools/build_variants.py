@@ -1,4 +1,4 @@
-"""Build LP-kernel tuning variants into scratch/ (bench with DLP_LIB_PATH=...)."""
+"""Build LP-kernel tuning variants into variants/ (A/B with tools/gpu/ab.sh or DLP_LIB_PATH=...)."""
 import os
 import sys
 
@@ -8,24 +8,18 @@ from paper_2604_06596_b200 import build  # noqa: E402
 VARIANTS = {
     "prev": [],  # the committed source (A/B against a working-tree change)
     "hubprof": ["DLP_HUBPROF"],
-    "minb2": ["DLP_LP_MINB=2"],
-    "minb2hp": ["DLP_LP_MINB=2", "DLP_HUBPROF"],
-    "minb4": ["DLP_LP_MINB=4"],
-    "minb4w32": ["DLP_LP_MINB=4", "DLP_WIN=32"],
+    "minb3": ["DLP_LP_MINB=3"],          # 3 CTAs/SM at 80 registers (spills)
     "w32": ["DLP_WIN=32"],
-    "w64": ["DLP_WIN=64"],
-    "sel": ["DLP_SUMS_SELECT"],
-    "pred": ["DLP_SUMS_PRED"],
-    "blkbr": ["DLP_BLOCK_BRANCH"],
-    "ca16": ["DLP_CP16_CA"],
-    "hw64": ["DLP_HUB_WIN=64"],
-    "blk8": ["DLP_ACC_UNROLL=8"],
-    "lp2": ["DLP_LONG_PER=2"],
-    "u2": ["DLP_ACC_UNROLL=2"],
+    "w96": ["DLP_WIN=96"],
     "u8": ["DLP_ACC_UNROLL=8"],
+    "rpl2": ["DLP_RPL2=1"],              # two rows per lane (measured slower)
+    "hubcta": ["DLP_HUB_CTA_ALWAYS"],    # hub rows on whole CTAs in every round
+    "hub1024": ["DLP_HUB_ROW_DEFAULT=1024"],
+    "long160": ["DLP_LONG_ROW_DEFAULT=160"],
+    "scan64": ["DLP_SCAN_RATIO=64"],
 }
 if __name__ == "__main__":
-    root = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "scratch")
+    root = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "variants")
     os.makedirs(root, exist_ok=True)
     only = sys.argv[1:]
     for name, d in VARIANTS.items():
