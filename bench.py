@@ -676,9 +676,10 @@ def main():
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": cfg["desc"], "points": cfg["n"], "timed_batches": f"t={t0}..{T - 1}",
                    "label_columns": ncol, "delta": delta,
-                   "parallelism": ((f"component-sharded x{world} (LPT placement, NCCL in the engine)"
-                                    if args.shard_mode != "rows" else
-                                    f"row-partitioned x{world} (per-round NCCL all-gather of packed rows)")
+                   "parallelism": ((f"component-sharded x{world} ({'LPT' if args.shard_mode == 'components' else 'hash'}"
+                                    f" placement, " if args.shard_mode != "rows" else
+                                    f"row-partitioned x{world} (per-round all-gather of packed rows, ")
+                                   + ("NCCL in the engine)" if nccl else "host collective)")
                                    if sharded else f"replicas x{world}"),
                    "l2": "no flush: each batch's working set (adjacency pool, edge log, label and staging "
                          "columns) exceeds the 126 MB L2"},
