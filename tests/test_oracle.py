@@ -133,3 +133,25 @@ def test_column_parallel_oracle_is_bitwise_serial():
         assert [(r.iterations, r.updates, r.max_change, r.edges_traversed) for r in ra] == \
             [(r.iterations, r.updates, r.max_change, r.edges_traversed) for r in rb], t
         assert a.labels()[0].tobytes() == b.labels()[0].tobytes(), t
+
+
+def test_c5_grid3d_knn_exact():
+    """C5's generator: exact 3-D Euclidean k-NN of uniform
+    cube points, union-symmetrised with max-merge, against brute force."""
+    import numpy as np
+
+    from paper_2604_06596_b200 import streams
+
+    b = streams.uniform_cube(3000, 2)
+    e = streams.knn_graph_grid3d(b.x, 10)
+    d2 = ((b.x[:, None, :] - b.x[None, :, :]) ** 2).sum(-1)
+    np.fill_diagonal(d2, np.inf)
+    nn = np.argsort(d2, axis=1, kind="stable")[:, :10]
+    pairs = set()
+    for i in range(len(b.x)):
+        for j in nn[i]:
+            pairs.add((min(i, int(j)), max(i, int(j))))
+    got = set(zip(e.u.tolist(), e.v.tolist()))
+    assert got == pairs
+    assert (e.w > 0).all() and (e.w <= 1).all()
+    assert set(np.unique(b.classes).tolist()) <= {0, 1}
