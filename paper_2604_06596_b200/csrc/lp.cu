@@ -55,7 +55,7 @@ constexpr int kLpThreads = 256;
 #define DLP_LABEL_WIN 64  // C-wide label rows staged per warp window (>= DLP_WIN)
 #endif
 #ifndef DLP_HUB_WIN
-#define DLP_HUB_WIN 128
+#define DLP_HUB_WIN 192  // hub window (entries); 128: +1.3-1.7% on C2
 #endif
 #ifndef DLP_LP_MINB
 #define DLP_LP_MINB 2
